@@ -167,6 +167,11 @@ class OracleEnv:
                                        _ptr(term), _ptr(trunc)))
         return obs, rew, done, term, trunc
 
+    def step_into(self, actions, obs, rew, done, term=None, trunc=None) -> None:
+        """Step writing into caller-provided (preallocated) numpy buffers."""
+        _check(lib().octax_oracle_step(self._h, _ptr(actions), _ptr(obs), _ptr(rew), _ptr(done),
+                                       _ptr(term), _ptr(trunc)))
+
     def stats(self):
         out = np.zeros(4, np.int64)
         rc = lib().octax_oracle_stats(self._h, _ptr(out))

@@ -1,0 +1,71 @@
+// octax_dev.cuh -- internal (non-ABI) structures shared by the host library and
+// the sm_100a kernels of the B200 Octax step.  Nothing here is shared with oracle/.
+#pragma once
+#include <cstdint>
+
+namespace octax {
+
+constexpr int kBlock = 128;          // envs (threads) per CTA
+constexpr int kFbStride = 33;        // u64 per env row block in smem (32 rows + 1 pad)
+constexpr int kMaxStartup = 32;
+constexpr int kMaxOps = 64;
+constexpr int kMaxDepth = 8;
+constexpr uint32_t kImageBytes = 4096;
+
+// expression bytecode (postfix, evaluated with top-of-stack in a register)
+enum ExprOp : uint8_t {
+  X_CONST = 0, X_V, X_I, X_DT, X_ST, X_MEM, X_NEG, X_NOT, X_BNOT,
+  X_MUL, X_DIV, X_MOD, X_ADD, X_SUB, X_SHL, X_SHR,
+  X_LT, X_LE, X_GT, X_GE, X_EQ, X_NE, X_AND, X_XOR, X_OR, X_LAND, X_LOR
+};
+
+struct ExprInsn {
+  uint8_t op;
+  uint8_t arg;
+  uint16_t pad;
+  uint32_t imm;
+};
+
+struct Program {
+  ExprInsn ops[kMaxOps];
+  uint32_t len;
+  uint32_t depth;
+};
+
+// Device-resident per-env state, structure-of-arrays (one entry per local env).
+struct DevState {
+  uint4 *regs;       // [n]    V0..VF, byte k of the 16 = Vk
+  uint4 *ctrl;       // [n]    {PC | I<<16, SP | DT<<8 | ST<<16 | halted<<24, draw, episode}
+  uint4 *book;       // [n]    {steps, prev_score, ep_ret, 0}
+  uint4 *stack;      // [n*2]  16 x u16 return addresses
+  uint64_t *dirty;   // [n]    copy-on-write block mask (64 blocks of 64 B)
+  uint8_t *ram;      // [n*4096] RAM backing; only dirty blocks are valid
+  uint64_t *ring;    // [n][4][32] display history, packed byte order (bswap of row)
+  unsigned long long *stats;  // [4] {returns, episodes, steps, err}
+  const uint8_t *image;       // [4096] pristine image: zeros, font at 0x50, ROM at 0x200
+};
+
+struct StepParams {
+  DevState s;
+  uint64_t n;
+  uint64_t env_offset;
+  uint64_t seed;
+  uint32_t head;          // ring slot holding the current display
+  uint32_t frame_skip;
+  uint32_t ipf;
+  uint32_t max_steps;
+  uint32_t quirks;
+  uint32_t obs_format;
+  uint32_t n_actions;     // n_action_keys + 1
+  uint32_t n_startup;
+  uint16_t keymask[17];   // action -> key mask
+  uint16_t pad0;
+  uint32_t startup_keys[kMaxStartup];
+  uint32_t startup_frames[kMaxStartup];
+  Program score;
+  Program term;
+};
+
+enum Mode : int { MODE_STEP = 0, MODE_RESET = 1 };
+
+}  // namespace octax

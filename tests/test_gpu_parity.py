@@ -1,0 +1,276 @@
+"""GPU <-> oracle parity (-m gpu).  The CUDA path (through the C ABI) must be
+BIT-EXACT against the CPU oracle: registers, RAM, framebuffer, history,
+observations, rewards, dones, episode statistics (integer work,
+so the tolerance is zero; rewards are small integers stored exactly in f32)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from tests.helpers import canon, hand_vectors
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _gpu_env(rom, spec, n, seed, offset=0):
+    from paper_2510_01764_b200 import OctaxEnv
+    return OctaxEnv(rom, spec, n, seed, env_offset=offset)
+
+
+def _step_both(g, o, acts):
+    a_dev = torch.from_numpy(acts).cuda()
+    obs, rew, done = g.step(a_dev)
+    term, trunc = g.terminated, g.truncated
+    oo, orw, od, ot, otr = o.step(acts)
+    return (obs.cpu().numpy().reshape(len(acts), -1), rew.cpu().numpy(), done.cpu().numpy(),
+            term.cpu().numpy(), trunc.cpu().numpy()), (oo, orw, od, ot, otr)
+
+
+def _assert_same(gout, oout, t):
+    names = ("obs", "reward", "done", "terminated", "truncated")
+    for name, a, b in zip(names, gout, oout):
+        if not np.array_equal(a, b):
+            bad = np.argwhere(a != b) if a.ndim > 1 else np.nonzero(a != b)[0]
+            raise AssertionError(f"step {t}: {name} differs at {bad[:5]}")
+
+
+def _assert_states(g, o, envs):
+    gs = g.get_states(envs)
+    for k, j in enumerate(envs):
+        os_ = o.get_state(j)
+        if not np.array_equal(gs[k], os_):
+            diff = np.nonzero(gs[k] != os_)[0]
+            raise AssertionError(f"env {j}: canonical state differs at bytes {diff[:12]} "
+                                 f"gpu={gs[k][diff[:12]]} oracle={os_[diff[:12]]}")
+
+
+def _run_parity(name_or_rom, spec, n, steps, seed, action_seed, check_every=25):
+    rom = workloads.rom_bytes(name_or_rom) if isinstance(name_or_rom, str) else name_or_rom
+    g = _gpu_env(rom, spec, n, seed)
+    o = oracle.OracleEnv(rom, spec, n, seed)
+    _assert_states(g, o, list(range(n)))
+    na = len(spec["action_keys"]) + 1
+    for t in range(steps):
+        acts = workloads.gen.actions(action_seed, t, n, na)
+        gout, oout = _step_both(g, o, acts)
+        _assert_same(gout, oout, t)
+        if (t + 1) % check_every == 0 or t == steps - 1:
+            _assert_states(g, o, list(range(n)))
+    gs, grc = g.stats()
+    os_, orc = o.stats()
+    assert np.array_equal(gs, os_) and grc == orc
+    return g, o
+
+
+# ---------------------------------------------------------------- config 1
+def test_coverage_rom_n1_1000_steps_full_state_every_step():
+    rom, spec = workloads.game("coverage")
+    g = _gpu_env(rom, spec, 1, workloads.ENV_SEED)
+    o = oracle.OracleEnv(rom, spec, 1, workloads.ENV_SEED)
+    for t in range(1000):
+        acts = workloads.gen.actions(1, t, 1, 17)
+        gout, oout = _step_both(g, o, acts)
+        _assert_same(gout, oout, t)
+        _assert_states(g, o, [0])
+    f = oracle.canon_fields(g.get_state(0))
+    assert f["mem"][0xF00] == 20 and np.all(f["mem"][0xF01:0xF15] == 0xA5)
+
+
+# ---------------------------------------------------------------- stand-in games, ragged n
+@pytest.mark.parametrize("game,n", [("pong_standin", 300), ("brix_standin", 257), ("brix_standin", 1)])
+def test_game_parity(game, n):
+    rom, spec = workloads.game(game)
+    _run_parity(rom, spec, n, 300, 77, 5)
+
+
+@pytest.mark.parametrize("fseed", list(range(8)))
+def test_fuzz_rom_parity(fseed):
+    rom = workloads.gen.fuzz_rom(fseed, n_instr=200 + 40 * fseed)
+    spec = dict(workloads.DEFAULTS, score="V0 + (V1 << 8) + mem[0x300]", terminated="0",
+                action_keys=list(range(16)), max_episode_steps=40 + 13 * fseed)
+    _run_parity(rom, spec, 160, 120, 1000 + fseed, fseed, check_every=20)
+
+
+@pytest.mark.parametrize("quirks", [1, 2, 4, 8, 16, 31])
+def test_quirk_parity(quirks):
+    rom = workloads.gen.fuzz_rom(100 + quirks, n_instr=300)
+    spec = dict(workloads.DEFAULTS, score="V5 * 3 - VF", terminated="VE == 7",
+                action_keys=[1, 2, 3, 12], quirks=quirks, max_episode_steps=60)
+    _run_parity(rom, spec, 130, 80, quirks, quirks)
+
+
+def test_bool_obs_startup_and_truncation_parity():
+    rom, spec = workloads.game("brix_standin", obs_format=1, startup=[(1 << 4, 7), (0, 3), (1 << 6, 2)],
+                               max_episode_steps=33)
+    _run_parity(rom, spec, 200, 100, 3, 3)
+
+
+def test_frame_skip_ipf_variants_parity():
+    rom, spec = workloads.game("pong_standin", frame_skip=1, instructions_per_frame=1)
+    _run_parity(rom, spec, 64, 200, 9, 9)
+    rom, spec = workloads.game("pong_standin", frame_skip=7, instructions_per_frame=31)
+    _run_parity(rom, spec, 64, 60, 9, 9)
+
+
+def test_reset_parity_and_obs():
+    rom, spec = workloads.game("pong_standin", startup=[(2, 5)])
+    g = _gpu_env(rom, spec, 50, 4)
+    o = oracle.OracleEnv(rom, spec, 50, 4)
+    for t in range(30):
+        _step_both(g, o, workloads.gen.actions(4, t, 50, 3))
+    go = g.reset(123).cpu().numpy().reshape(50, -1)
+    oo = o.reset(123)
+    assert np.array_equal(go, oo)
+    _assert_states(g, o, list(range(50)))
+    gs, _ = g.stats()
+    assert list(gs) == [0, 0, 0, 0]
+
+
+def test_out_of_range_actions_flag():
+    rom, spec = workloads.game("pong_standin")
+    g = _gpu_env(rom, spec, 40, 1)
+    o = oracle.OracleEnv(rom, spec, 40, 1)
+    acts = workloads.gen.actions(2, 0, 40, 3)
+    acts[3], acts[17] = 9, -4
+    gout, oout = _step_both(g, o, acts)
+    _assert_same(gout, oout, 0)
+    gs, grc = g.stats()
+    os_, orc = o.stats()
+    assert grc == orc == -8 and np.array_equal(gs, os_)
+
+
+# ---------------------------------------------------------------- single instructions
+@pytest.mark.parametrize("word,init,exp", list(hand_vectors()))
+def test_hand_vector_parity(word, init, exp):
+    """Each hand vector as a one-cycle step (fs=1, ipf=1) on both sides."""
+    spec = dict(workloads.DEFAULTS, score="0", terminated="0", action_keys=list(range(16)),
+                frame_skip=1, instructions_per_frame=1)
+    rom = bytes([0x12, 0x00])
+    g = _gpu_env(rom, spec, 1, 42)
+    o = oracle.OracleEnv(rom, spec, 1, 42)
+    f = oracle.canon_fields(o.get_state(0))
+    mem = f["mem"]
+    mem[0x300], mem[0x301] = word >> 8, word & 0xFF
+    V = [0] * 16
+    for k in range(16):
+        V[k] = init.get(f"V{k:X}", init.get(f"V{k}", 0))
+    stack = [init.get("STK0", 0)] + [0] * 15
+    c = canon(V=V, I=init.get("I", 0), PC=0x300, SP=init.get("SP", 0), DT=init.get("DT", 0),
+              ST=init.get("ST", 0), stack=stack, mem=mem, display=f["display"], hist=f["hist"])
+    g.set_state(0, c)
+    o.set_state(0, c)
+    keys = init.get("KEYS", 0)
+    action = 0 if keys == 0 else (keys & -keys).bit_length()  # key k -> action k+1
+    acts = np.array([action], np.int32)
+    gout, oout = _step_both(g, o, acts)
+    _assert_same(gout, oout, 0)
+    _assert_states(g, o, [0])
+
+
+def test_set_get_state_roundtrip_random():
+    rng = np.random.default_rng(5)
+    rom, spec = workloads.game("pong_standin")
+    g = _gpu_env(rom, spec, 3, 1)
+    for _ in range(20):
+        c = rng.integers(0, 256, 5200, dtype=np.uint8)
+        c[20] = rng.integers(0, 17)
+        c[23] &= 1
+        c[76:80] = 0
+        g.set_state(1, c)
+        assert np.array_equal(g.get_state(1), c)
+
+
+# ---------------------------------------------------------------- expressions
+EXPRS = ["V5", "(V14 // 10) - (V14 % 10)", "(V9 == 0) | (V12 >= 0x3E)", "V1 == 2",
+         "mem[I] + mem[I + 1] * 256", "-V3 ^ ~V4", "V1 << V2 | V3 >> V4", "V1 / V2 + V3 % V4",
+         "!(V1 && V2) || V3 < V4 && V5 >= V6", "DT * ST - I", "mem[V0 * 16 + V1]",
+         "((V1 + 2) * (V2 + 3) - (V3 + 4) * (V4 + 5)) / (V6 - V7 + 1)"]
+
+
+@pytest.mark.parametrize("expr", EXPRS)
+def test_expression_parity(expr):
+    spec = dict(workloads.DEFAULTS, score=expr, terminated=expr, action_keys=[1],
+                frame_skip=1, instructions_per_frame=1, max_episode_steps=0)
+    rom = bytes([0x12, 0x00])
+    n = 64
+    g = _gpu_env(rom, spec, n, 1)
+    rng = np.random.default_rng(abs(hash(expr)) % 2**32)
+    base = oracle.canon_fields(g.get_state(0))
+    for j in range(n):
+        V = rng.integers(0, 256, 16)
+        V[rng.integers(0, 16)] = 0
+        mem = base["mem"].copy()
+        mem[0x300:0x400] = rng.integers(0, 256, 256, dtype=np.uint8)
+        c = canon(V=V, I=int(rng.integers(0, 0x10000)), PC=0x200, DT=int(rng.integers(0, 256)),
+                  ST=int(rng.integers(0, 256)), mem=mem, display=base["display"], hist=base["hist"])
+        g.set_state(j, c)
+    g.step(torch.zeros(n, dtype=torch.int32, device="cuda"))
+    st = g.get_states(list(range(n)))
+    term = g.terminated.cpu().numpy()
+    for j in range(n):
+        f = oracle.canon_fields(st[j])
+        # re-evaluate on the post-step state (timers ticked once) with the oracle's parser
+        want = oracle.eval_expr(expr, st[j])
+        assert f["prev_score"] == want, (j, f["prev_score"], want)
+        assert term[j] == (1 if want != 0 else 0)
+
+
+# ---------------------------------------------------------------- sharding / generator
+def test_shard_invariance_gpu():
+    rom, spec = workloads.game("pong_standin")
+    full = _gpu_env(rom, spec, 256, 8, 0)
+    lo = _gpu_env(rom, spec, 128, 8, 0)
+    hi = _gpu_env(rom, spec, 128, 8, 128)
+    a = torch.empty(256, dtype=torch.int32, device="cuda")
+    for t in range(50):
+        full.gen_actions(31, t, a)
+        full.step(a)
+        lo.step(a[:128].contiguous())
+        hi.step(a[128:].contiguous())
+    s = full.get_states(list(range(256)))
+    assert np.array_equal(s[:128], lo.get_states(list(range(128))))
+    assert np.array_equal(s[128:], hi.get_states(list(range(128))))
+
+
+def test_gen_actions_matches_oracle_generator():
+    rom, spec = workloads.game("coverage")
+    g = _gpu_env(rom, spec, 1000, 1, 5000)
+    a = torch.empty(1000, dtype=torch.int32, device="cuda")
+    for t in (0, 1, 2**32 + 7):
+        g.gen_actions(0xABCDEF0123, t, a)
+        want = oracle.synthetic_actions(0xABCDEF0123, t, range(5000, 6000), 17)
+        assert np.array_equal(a.cpu().numpy(), want)
+
+
+# ---------------------------------------------------------------- full size, bench launch config
+@pytest.mark.slow
+def test_full_size_sampled_parity():
+    """n = 1,048,576 (bench workload), device-generated actions, 64 sampled envs
+    re-simulated one by one by the oracle (SURVEY d.1 config 4 sampling)."""
+    rom, spec = workloads.game("pong_standin")
+    n, T = 1 << 20, 40
+    g = _gpu_env(rom, spec, n, workloads.ENV_SEED)
+    a = torch.empty(n, dtype=torch.int32, device="cuda")
+    key = [workloads.ENV_SEED & 0xFFFFFFFF, workloads.ENV_SEED >> 32]
+    ids = [0, 1, n // 2, n - 1] + [oracle.philox4x32_10([k, 0, 0, 2], key)[0] % n for k in range(60)]
+    oracles = [oracle.OracleEnv(rom, spec, 1, workloads.ENV_SEED, gid) for gid in ids]
+    idx = torch.tensor(ids, device="cuda")
+    for t in range(T):
+        g.gen_actions(workloads.ACTION_SEED, t, a)
+        obs, rew, done = g.step(a)
+        go = obs.reshape(n, -1)[idx].cpu().numpy()
+        gr = rew[idx].cpu().numpy()
+        gd = done[idx].cpu().numpy()
+        for k, gid in enumerate(ids):
+            act = np.array([oracle.synthetic_action(workloads.ACTION_SEED, t, gid, 3)], np.int32)
+            oo, orw, od, _, _ = oracles[k].step(act)
+            assert np.array_equal(go[k], oo[0]) and gr[k] == orw[0] and gd[k] == od[0], (t, gid)
+    st = g.get_states(ids)
+    for k in range(len(ids)):
+        assert np.array_equal(st[k], oracles[k].get_state(0))
+    s, _ = g.stats()
+    assert s[2] == n * T
