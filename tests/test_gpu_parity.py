@@ -4,6 +4,8 @@ observations, rewards, dones, episode statistics (integer work,
 so the tolerance is zero; rewards are small integers stored exactly in f32)."""
 from __future__ import annotations
 
+import zlib
+
 import numpy as np
 import pytest
 
@@ -193,13 +195,19 @@ EXPRS = ["V5", "(V14 // 10) - (V14 % 10)", "(V9 == 0) | (V12 >= 0x3E)", "V1 == 2
 
 @pytest.mark.parametrize("expr", EXPRS)
 def test_expression_parity(expr):
-    spec = dict(workloads.DEFAULTS, score=expr, terminated=expr, action_keys=[1],
-                frame_skip=1, instructions_per_frame=1, max_episode_steps=0)
+    """score: prev_score after the step must equal the oracle's parser evaluated on
+    the GPU's own post-step state; terminated: GPU and oracle run the same step
+    from the same random state and must agree on terminated (and everything else)."""
     rom = bytes([0x12, 0x00])
     n = 64
-    g = _gpu_env(rom, spec, n, 1)
-    rng = np.random.default_rng(abs(hash(expr)) % 2**32)
-    base = oracle.canon_fields(g.get_state(0))
+    rng = np.random.default_rng(zlib.crc32(expr.encode()))
+    spec_s = dict(workloads.DEFAULTS, score=expr, terminated="0", action_keys=[1],
+                  frame_skip=1, instructions_per_frame=1, max_episode_steps=0)
+    spec_t = dict(spec_s, score="0", terminated=expr)
+    gs_ = _gpu_env(rom, spec_s, n, 1)
+    gt = _gpu_env(rom, spec_t, n, 1)
+    ot = oracle.OracleEnv(rom, spec_t, n, 1)
+    base = oracle.canon_fields(gs_.get_state(0))
     for j in range(n):
         V = rng.integers(0, 256, 16)
         V[rng.integers(0, 16)] = 0
@@ -207,16 +215,17 @@ def test_expression_parity(expr):
         mem[0x300:0x400] = rng.integers(0, 256, 256, dtype=np.uint8)
         c = canon(V=V, I=int(rng.integers(0, 0x10000)), PC=0x200, DT=int(rng.integers(0, 256)),
                   ST=int(rng.integers(0, 256)), mem=mem, display=base["display"], hist=base["hist"])
-        g.set_state(j, c)
-    g.step(torch.zeros(n, dtype=torch.int32, device="cuda"))
-    st = g.get_states(list(range(n)))
-    term = g.terminated.cpu().numpy()
+        gs_.set_state(j, c)
+        gt.set_state(j, c)
+        ot.set_state(j, c)
+    gs_.step(torch.zeros(n, dtype=torch.int32, device="cuda"))
+    st = gs_.get_states(list(range(n)))
     for j in range(n):
-        f = oracle.canon_fields(st[j])
-        # re-evaluate on the post-step state (timers ticked once) with the oracle's parser
         want = oracle.eval_expr(expr, st[j])
-        assert f["prev_score"] == want, (j, f["prev_score"], want)
-        assert term[j] == (1 if want != 0 else 0)
+        assert oracle.canon_fields(st[j])["prev_score"] == want, j
+    gout, oout = _step_both(gt, ot, np.zeros(n, np.int32))
+    _assert_same(gout, oout, 0)
+    _assert_states(gt, ot, list(range(n)))
 
 
 # ---------------------------------------------------------------- sharding / generator
