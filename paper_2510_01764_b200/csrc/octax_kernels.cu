@@ -6,15 +6,20 @@
 //   * a warp-cooperative prologue streams the three previous display planes
 //     of its 32 envs from the HBM ring straight into obs planes 0..2
 //     (coalesced 256 B per env-plane) and the newest one into the shared-memory
-//     framebuffer (32 x u64 rows per env, padded to 33 to stay bank-conflict
-//     free);
-//   * each lane interprets frame_skip x instructions_per_frame CHIP-8 cycles
-//     (P:142-146), V0..VF in shared memory ([16][128] u32: any V[x] access by
-//     any lane mix is conflict free), DXYN as 64-bit XOR row ops on the smem
-//     framebuffer, RAM reads from the smem image unless the
-//     64-B block is dirty (copy-on-write overlay in HBM);
+//     framebuffer (32 x u64 rows per env, XOR-swizzled: bank-conflict free both
+//     for "one row of 32 envs" and "32 rows of one env" access);
+//   * the interpreter loop (frame_skip x instructions_per_frame cycles,
+//     P:142-146) is WARP-UNIFORM: every lane runs the same straight-line,
+//     predicated core for the cheap opcode classes (no divergent dispatch
+//     tree), and the rare / heavy classes (DXYN, CXNN, 00E0, FX33/55/65,
+//     dirty-RAM fetch) are vote-gated blocks executed once per warp when any
+//     lane needs them;
+//   * DXYN is drawn cooperatively: the sprite rows of all drawing lanes are
+//     spread over the 32 lanes (prefix sum + binary search on shuffles), each
+//     lane XORs one 64-bit framebuffer row, and the collision flags are
+//     gathered with one __reduce_or_sync;
 //   * score / termination bytecode -> reward, done; same-step
-//     auto-reset with startup segments (A10);
+//     auto-reset with startup segments (A10), also warp-uniform;
 //   * a warp-cooperative epilogue writes obs plane 3 and the new ring slot;
 //   * per-CTA integer episode statistics -> 4 int64 atomics per CTA.
 // Semantics follow DESIGN.md readings A1..A27; nothing here is shared with
@@ -27,17 +32,25 @@
 
 namespace octax {
 
+constexpr unsigned kFull = 0xffffffffu;
+constexpr uint32_t kLaneDrawMax = 8;  // rows: lane-parallel DXYN up to this, cooperative above
+
 struct __align__(128) Smem {
   uint8_t img[kImageBytes];                  // pristine image (TMA destination)
-  uint64_t fb[kBlock * kFbStride];           // framebuffer rows, bit 63-x = pixel x
+  uint64_t fb[kBlock * 32];                  // framebuffer rows, bit 63-x = pixel x, swizzled
   uint32_t V[16 * kBlock];                   // V[k*kBlock + tid]
   uint16_t stk[16 * kBlock];                 // stk[k*kBlock + tid]
   uint32_t evs[kMaxDepth * kBlock];          // expression stack (below top)
+  uint32_t dprm[kBlock / 32][32];            // DXYN owner params (x0 | y0 << 6 | base << 11)
+  uint8_t down[kBlock / 32][32];             // DXYN item -> owner lane map
   unsigned long long red[4][kBlock / 32];    // per-warp statistics
   unsigned long long bar;                    // mbarrier for the image copy
 };
 
 size_t smem_bytes() { return sizeof(Smem); }
+
+// framebuffer row `r` of CTA-local env `e`: XOR swizzle on the low 4 row bits
+__device__ __forceinline__ uint32_t fb_idx(uint32_t e, uint32_t r) { return e * 32u + (r ^ (e & 15u)); }
 
 __device__ __forceinline__ uint64_t bswap64(uint64_t v) {
   uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
@@ -88,13 +101,12 @@ __device__ __forceinline__ void image_load_wait(Smem &sm) {
 // ---------------------------------------------------------------- lane state
 struct Lane {
   uint32_t pc, I, sp, dt, st, halted, keys, draw, episode;
-  uint64_t dirty;
+  uint64_t dirty;   // copy-on-write mask: block b (64 B) of RAM lives in HBM
   uint8_t *ram;
   uint32_t stk_dirty;
 };
 
 #define VREG(k) sm.V[(k)*kBlock + tid]
-#define FBROW(r) sm.fb[tid * kFbStride + (r)]
 
 __device__ __forceinline__ uint32_t rd(const Smem &sm, const Lane &L, uint32_t a) {
   return ((L.dirty >> (a >> 6)) & 1ull) ? (uint32_t)L.ram[a] : (uint32_t)sm.img[a];
@@ -117,147 +129,266 @@ __device__ __forceinline__ void power_on(Smem &sm, Lane &L, int tid) {
 #pragma unroll
   for (int k = 0; k < 16; ++k) sm.stk[k * kBlock + tid] = 0;
 #pragma unroll
-  for (int r = 0; r < 32; ++r) FBROW(r) = 0;
+  for (int r = 0; r < 32; ++r) sm.fb[tid * 32 + r] = 0;
   L.pc = 0x200; L.I = 0; L.sp = 0; L.dt = 0; L.st = 0; L.halted = 0; L.keys = 0; L.draw = 0;
   L.dirty = 0;
   L.stk_dirty = 1;
 }
 
-// DXYN: XOR sprite rows into the framebuffer, VF = any lit pixel turned off.
-__device__ __forceinline__ void draw(Smem &sm, Lane &L, int tid, uint32_t x, uint32_t y, uint32_t n,
-                                     bool wrap) {
-  uint32_t x0 = VREG(x) & 63u, y0 = VREG(y) & 31u, base = L.I & 0xFFFu;
-  uint64_t hit = 0;
-  for (uint32_t r = 0; r < n; ++r) {
-    uint32_t yy = y0 + r;
-    if (yy >= 32u) {
-      if (!wrap) break;
-      yy &= 31u;
-    }
-    uint32_t a = base + r;
-    uint32_t byte = a <= 0xFFFu ? rd(sm, L, a) : 0u;
-    uint64_t m = (uint64_t)byte << 56;
-    m = wrap ? ((m >> x0) | (x0 ? (m << (64u - x0)) : 0ull)) : (m >> x0);
-    uint64_t old = FBROW(yy);
-    hit |= old & m;
-    FBROW(yy) = old ^ m;
+// Cooperative DXYN for every lane with do_draw (must be called by all 32 lanes).
+// Work item k of the warp = row r of owner lane j.  Row counts are prefix-summed
+// with 4 ballots (counts are 4-bit), owners publish (lane, params) into a per-warp
+// smem map at their start item, and each item finds its owner as the highest
+// start bit at or below it (one REDUX.OR + FLO), so a pass costs no shuffle chain.
+__device__ __forceinline__ void draw_coop(Smem &sm, const Lane &L, const StepParams &p, int tid, int lane,
+                                          uint64_t block0, bool do_draw, uint32_t x0, uint32_t y0, uint32_t base,
+                                          uint32_t n) {
+  const bool wrap = (p.quirks & 8u) != 0;
+  const uint32_t nrows = do_draw ? (wrap ? n : min(n, 32u - y0)) : 0u;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t excl = 0, total = 0;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const uint32_t B = __ballot_sync(kFull, (nrows >> b) & 1u);
+    excl += (uint32_t)__popc(B & lt) << b;
+    total += (uint32_t)__popc(B) << b;
   }
-  VREG(15) = hit ? 1u : 0u;
+  const uint32_t warp = (uint32_t)tid >> 5, wl = (uint32_t)tid & ~31u;
+  sm.dprm[warp][lane] = x0 | (y0 << 6) | (base << 11);
+  uint32_t hitmask = 0;
+  for (uint32_t b0 = 0; b0 < total; b0 += 32) {
+    const bool inw = nrows != 0u && excl >= b0 && excl < b0 + 32u;
+    if (inw) sm.down[warp][excl - b0] = (uint8_t)lane;
+    const uint32_t M = __reduce_or_sync(kFull, inw ? 1u << (excl - b0) : 0u);
+    const uint32_t cover = __ballot_sync(kFull, nrows != 0u && excl < b0 && excl + nrows > b0);
+    const uint32_t cj = cover ? (uint32_t)(__ffs(cover) - 1) : 0u;
+    const uint32_t cex = __shfl_sync(kFull, excl, cj);
+    __syncwarp();
+    const uint32_t k = b0 + (uint32_t)lane;
+    const uint32_t mk = M & (0xFFFFFFFFu >> (31 - lane));
+    uint32_t j, r;
+    if (mk) {
+      const uint32_t pos = 31u - (uint32_t)__clz(mk);
+      j = sm.down[warp][pos];
+      r = (uint32_t)lane - pos;
+    } else {
+      j = cj;
+      r = k - cex;
+    }
+    const uint64_t dj = __shfl_sync(kFull, L.dirty, j);
+    bool hit = false;
+    if (k < total) {
+      const uint32_t pj = sm.dprm[warp][j];
+      const uint32_t xj = pj & 63u, yy = (((pj >> 6) & 31u) + r) & 31u, a = (pj >> 11) + r;
+      uint32_t byte = 0;
+      if (a <= 0xFFFu)
+        byte = ((dj >> (a >> 6)) & 1ull) ? (uint32_t)p.s.ram[(block0 + wl + j) * 4096ull + a] : (uint32_t)sm.img[a];
+      uint64_t m = (uint64_t)byte << 56;
+      m = bswap64(wrap ? ((m >> xj) | (xj ? (m << (64u - xj)) : 0ull)) : (m >> xj));
+      uint64_t *row = &sm.fb[fb_idx(wl + j, yy)];
+      const uint64_t old = *row;
+      *row = old ^ m;
+      hit = (old & m) != 0ull;
+    }
+    hitmask |= __reduce_or_sync(kFull, hit ? (1u << j) : 0u);
+    __syncwarp();
+  }
+  if (do_draw) VREG(15) = (hitmask >> lane) & 1u;
 }
 
-__device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, int tid, uint32_t gid) {
-  if (L.pc > 0xFFEu) { L.halted = 1; return; }
-  uint32_t op = (rd(sm, L, L.pc) << 8) | rd(sm, L, L.pc + 1);
-  L.pc = (L.pc + 2) & 0xFFFFu;
-  uint32_t x = (op >> 8) & 15u, y = (op >> 4) & 15u, n = op & 15u, nn = op & 255u, nnn = op & 0xFFFu;
-  switch (op >> 12) {
-    case 0x0:
-      if (op == 0x00E0u) {
-#pragma unroll
-        for (int r = 0; r < 32; ++r) FBROW(r) = 0;
-      } else if (op == 0x00EEu) {
-        if (L.sp == 0) { L.halted = 1; return; }
-        L.sp--;
-        L.pc = sm.stk[L.sp * kBlock + tid];
-      }
-      break;
-    case 0x1: L.pc = nnn; break;
-    case 0x2:
-      if (L.sp == 16) { L.halted = 1; return; }
-      sm.stk[L.sp * kBlock + tid] = (uint16_t)L.pc;
-      L.sp++;
-      L.stk_dirty = 1;
-      L.pc = nnn;
-      break;
-    case 0x3: if (VREG(x) == nn) L.pc += 2; break;
-    case 0x4: if (VREG(x) != nn) L.pc += 2; break;
-    case 0x5:
-      if (n) { L.halted = 1; return; }
-      if (VREG(x) == VREG(y)) L.pc += 2;
-      break;
-    case 0x6: VREG(x) = nn; break;
-    case 0x7: VREG(x) = (VREG(x) + nn) & 255u; break;
-    case 0x8: {
-      uint32_t a = VREG(x), b = VREG(y), r, f;
-      bool vf_reset = (p.quirks & 16u) != 0;
-      uint32_t s = (p.quirks & 1u) ? b : a;
-      switch (n) {
-        case 0x0: VREG(x) = b; return;
-        case 0x1: VREG(x) = a | b; if (vf_reset) VREG(15) = 0; return;
-        case 0x2: VREG(x) = a & b; if (vf_reset) VREG(15) = 0; return;
-        case 0x3: VREG(x) = a ^ b; if (vf_reset) VREG(15) = 0; return;
-        case 0x4: r = a + b; f = r >> 8; r &= 255u; break;
-        case 0x5: r = (a - b) & 255u; f = a >= b; break;
-        case 0x6: r = s >> 1; f = s & 1u; break;
-        case 0x7: r = (b - a) & 255u; f = b >= a; break;
-        case 0xE: r = (s << 1) & 255u; f = s >> 7; break;
-        default: L.halted = 1; return;
-      }
-      VREG(x) = r;
-      VREG(15) = f;  // flag written last (A15)
-      break;
+// DXYN, lane-parallel: every drawing lane XORs its own rows, loop bound = the
+// warp's largest row count (uniform).  Fast variants (sprite bytes from the smem
+// image, clip or wrap) are branch-free: rows past a lane's count XOR a zero mask
+// into its own (lane-private) rows.  Any dirty sprite block -> general loop.
+// The framebuffer holds rows in packed byte order (byte b = pixels 8b..8b+7, MSB
+// leftmost), so the mask is built as bswap16(sprite << 8 >> (x0 & 7)) << 8*(x0 >> 3).
+__device__ __forceinline__ void draw_lanes(Smem &sm, Lane &L, const StepParams &p, int tid, bool do_draw,
+                                           uint32_t x0, uint32_t y0, uint32_t base, uint32_t nrows, uint32_t maxr) {
+  const bool wrap = (p.quirks & 8u) != 0;
+  const bool slowb = do_draw & ((((L.dirty >> (base >> 6)) & 3ull) != 0ull) | (base + 15u > 0xFFFu));
+  const uint32_t sh = x0 & 7u, q8 = (x0 >> 3) * 8u, swz = (uint32_t)tid & 15u;
+  uint64_t *rows = &sm.fb[(uint32_t)tid * 32u];
+  const uint8_t *spr = sm.img + (base & 0xFFFu);
+  uint64_t hit = 0;
+  if (__any_sync(kFull, slowb)) {
+    for (uint32_t r = 0; r < maxr; ++r) {
+      const uint32_t a = base + r;
+      uint32_t byte = (r < nrows && a <= 0xFFFu) ? rd(sm, L, a) : 0u;
+      const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> sh, 0, 0x4401);
+      const uint64_t m = wrap ? ((w << q8) | (q8 ? (w >> (64u - q8)) : 0ull)) : (w << q8);
+      uint64_t *row = rows + (((y0 + r) & 31u) ^ swz);
+      const uint64_t old = *row;
+      *row = old ^ m;
+      hit |= old & m;
     }
-    case 0x9:
-      if (n) { L.halted = 1; return; }
-      if (VREG(x) != VREG(y)) L.pc += 2;
-      break;
-    case 0xA: L.I = nnn; break;
-    case 0xB: L.pc = (nnn + VREG((p.quirks & 4u) ? x : 0u)) & 0xFFFu; break;
-    case 0xC: {
-      uint32_t r = philox_out0(L.draw, L.episode, gid, 0u, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
+  } else if (!wrap) {
+    for (uint32_t r = 0; r < maxr; ++r) {
+      const uint32_t byte = r < nrows ? (uint32_t)spr[r] : 0u;
+      const uint64_t m = (uint64_t)__byte_perm((byte << 8) >> sh, 0, 0x4401) << q8;
+      uint64_t *row = rows + (((y0 + r) & 31u) ^ swz);
+      const uint64_t old = *row;
+      *row = old ^ m;
+      hit |= old & m;
+    }
+  } else {
+    for (uint32_t r = 0; r < maxr; ++r) {
+      const uint32_t byte = r < nrows ? (uint32_t)spr[r] : 0u;
+      const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> sh, 0, 0x4401);
+      const uint64_t m = (w << q8) | (q8 ? (w >> (64u - q8)) : 0ull);
+      uint64_t *row = rows + (((y0 + r) & 31u) ^ swz);
+      const uint64_t old = *row;
+      *row = old ^ m;
+      hit |= old & m;
+    }
+  }
+  if (do_draw) VREG(15) = hit != 0ull;
+}
+
+// One CHIP-8 cycle for every lane with `part` (must be called by all 32 lanes).
+// Branch-free predicated core; class tests are one-hot masks cm = 1 << (op >> 12).
+__device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, int tid, int lane, uint64_t block0,
+                                      uint32_t gid, bool part) {
+  bool act = part & (L.halted == 0u);
+  const uint32_t pc = L.pc;
+  const bool oob = pc > 0xFFEu;
+  // ---- fetch: one 8-byte load from the smem image (slow path: dirty block or straddle)
+  const uint64_t w8 = *reinterpret_cast<const uint64_t *>(sm.img + (pc & 0xFF8u));
+  uint32_t op = __byte_perm((uint32_t)(w8 >> ((pc & 7u) * 8u)), 0, 0x4401);
+  const bool slow = act & !oob & (((pc & 7u) == 7u) | (((L.dirty >> (pc >> 6)) & 1ull) != 0ull));
+  if (__any_sync(kFull, slow)) {
+    if (slow) op = (rd(sm, L, pc) << 8) | rd(sm, L, pc + 1);
+  }
+  // ---- decode
+  const uint32_t hi = op >> 12, cm = 1u << hi, x = (op >> 8) & 15u, y = (op >> 4) & 15u, n = op & 15u,
+                 nn = op & 255u, nnn = op & 0xFFFu;
+  const uint32_t vx = VREG(x), vy = VREG(y);
+  const bool isF = hi == 0xFu;
+  const bool f07 = isF & (nn == 0x07u), f0a = isF & (nn == 0x0Au), f15 = isF & (nn == 0x15u),
+             f18 = isF & (nn == 0x18u), f1e = isF & (nn == 0x1Eu), f29 = isF & (nn == 0x29u),
+             f33 = isF & (nn == 0x33u), f55 = isF & (nn == 0x55u), f65 = isF & (nn == 0x65u);
+  const bool is_ret = op == 0x00EEu, is_cls = op == 0x00E0u, is_call = hi == 2u;
+  const bool c59 = (cm & 0x0220u) != 0u;  // 5XY0 / 9XY0
+  // ---- faults halt the lane (A17, A20)
+  bool bad = oob;
+  bad |= c59 & (n != 0u);
+  bad |= (hi == 8u) & (n > 7u) & (n != 0xEu);
+  bad |= (hi == 0xEu) & (nn != 0x9Eu) & (nn != 0xA1u);
+  bad |= isF & !(f07 | f0a | f15 | f18 | f1e | f29 | f33 | f55 | f65);
+  bad |= is_ret & (L.sp == 0u);
+  bad |= is_call & (L.sp == 16u);
+  L.halted |= (uint32_t)(act & bad);
+  act = act & !bad;
+  // ---- stack
+  uint32_t ret_pc = 0;
+  if (act & is_ret) ret_pc = sm.stk[(L.sp - 1u) * kBlock + tid];
+  if (act & is_call) { sm.stk[L.sp * kBlock + tid] = (uint16_t)(pc + 2u); L.stk_dirty = 1; }
+  // ---- skips: 3XNN 5XY0 on equal, 4XNN 9XY0 on not-equal, EX9E / EXA1 on key
+  const bool eq = vx == (c59 ? vy : nn);
+  const bool keyd = ((L.keys >> (vx & 15u)) & 1u) != 0u;
+  const bool skip = (((cm & 0x0028u) != 0u) & eq) | (((cm & 0x0210u) != 0u) & !eq) |
+                    ((hi == 0xEu) & (keyd ^ (nn == 0xA1u)));
+  // ---- ALU 8XYn; flag written after the result (A15)
+  const uint32_t s = (p.quirks & 1u) ? vy : vx;
+  const bool sub5 = n == 5u, sub7 = n == 7u;
+  const uint32_t sa = sub7 ? vy : vx;
+  uint32_t sb = vy;
+  sb = sub5 ? (vy ^ 255u) : sb;
+  sb = sub7 ? (vx ^ 255u) : sb;
+  const uint32_t sum = sa + sb + (uint32_t)(sub5 | sub7);
+  uint32_t r8 = vy, f8 = 0u;
+  r8 = (n == 1u) ? (vx | vy) : r8;
+  r8 = (n == 2u) ? (vx & vy) : r8;
+  r8 = (n == 3u) ? (vx ^ vy) : r8;
+  const bool add = (n == 4u) | sub5 | sub7;
+  r8 = add ? (sum & 255u) : r8;
+  f8 = add ? (sum >> 8) : f8;
+  r8 = (n == 6u) ? (s >> 1) : r8;
+  f8 = (n == 6u) ? (s & 1u) : f8;
+  r8 = (n == 0xEu) ? ((s << 1) & 255u) : r8;
+  f8 = (n == 0xEu) ? (s >> 7) : f8;
+  const bool is8 = hi == 8u;
+  const bool wvf = act & is8 & ((n >= 4u) | (((p.quirks & 16u) != 0u) & (n >= 1u)));
+  // ---- register writes
+  uint32_t nvx = nn;
+  nvx = (hi == 7u) ? ((vx + nn) & 255u) : nvx;
+  nvx = is8 ? r8 : nvx;
+  nvx = f07 ? L.dt : nvx;
+  nvx = f0a ? (uint32_t)(__ffs(L.keys) - 1) : nvx;
+  const bool wvx = act & (((cm & 0x01C0u) != 0u) | f07 | (f0a & (L.keys != 0u)));
+  if (wvx) VREG(x) = nvx;
+  if (wvf) VREG(15) = f8;
+  // ---- control flow and index / timer registers
+  uint32_t npc = pc + (skip ? 4u : 2u);
+  npc = ((cm & 0x0006u) != 0u) ? nnn : npc;  // 1NNN, 2NNN
+  npc = is_ret ? ret_pc : npc;
+  npc = (f0a & (L.keys == 0u)) ? pc : npc;   // A16: FX0A re-executes while no key
+  if (act & (hi == 0xBu)) npc = (nnn + VREG((p.quirks & 4u) ? x : 0u)) & 0xFFFu;
+  uint32_t I2 = L.I;
+  I2 = (hi == 0xAu) ? nnn : I2;
+  I2 = f1e ? ((I2 + vx) & 0xFFFFu) : I2;
+  I2 = f29 ? (0x50u + 5u * (vx & 15u)) : I2;
+  if (act) {
+    L.pc = npc & 0xFFFFu;
+    L.I = I2;
+    L.sp = L.sp + (uint32_t)is_call - (uint32_t)is_ret;
+    L.dt = f15 ? vx : L.dt;
+    L.st = f18 ? vx : L.st;
+  }
+  // ---- vote-gated rare classes
+  const bool do_cls = act & is_cls;
+  if (__any_sync(kFull, do_cls)) {
+    if (do_cls) {
+#pragma unroll
+      for (int r = 0; r < 32; ++r) sm.fb[tid * 32 + r] = 0;
+    }
+  }
+  const bool do_rnd = act & (hi == 0xCu);
+  if (__any_sync(kFull, do_rnd)) {
+    if (do_rnd) {
+      const uint32_t r = philox_out0(L.draw, L.episode, gid, 0u, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
       VREG(x) = r & nn & 255u;
       L.draw++;
-      break;
     }
-    case 0xD: draw(sm, L, tid, x, y, n, (p.quirks & 8u) != 0); break;
-    case 0xE: {
-      uint32_t down = (L.keys >> (VREG(x) & 15u)) & 1u;
-      if (nn == 0x9Eu) { if (down) L.pc += 2; }
-      else if (nn == 0xA1u) { if (!down) L.pc += 2; }
-      else { L.halted = 1; return; }
-      break;
-    }
-    default: {  // 0xF
-      switch (nn) {
-        case 0x07: VREG(x) = L.dt; break;
-        case 0x0A:
-          if (L.keys) VREG(x) = __ffs(L.keys) - 1;
-          else L.pc -= 2;
-          break;
-        case 0x15: L.dt = VREG(x); break;
-        case 0x18: L.st = VREG(x); break;
-        case 0x1E: L.I = (L.I + VREG(x)) & 0xFFFFu; break;
-        case 0x29: L.I = 0x50u + 5u * (VREG(x) & 15u); break;
-        case 0x33: {
-          uint32_t v = VREG(x);
-          wr(sm, L, L.I & 0xFFFu, v / 100u);
-          wr(sm, L, (L.I + 1u) & 0xFFFu, (v / 10u) % 10u);
-          wr(sm, L, (L.I + 2u) & 0xFFFu, v % 10u);
-          break;
-        }
-        case 0x55:
+  }
+  const bool do_mem = act & (f33 | f55 | f65);
+  if (__any_sync(kFull, do_mem)) {
+    if (do_mem) {
+      if (f33) {
+        wr(sm, L, L.I & 0xFFFu, vx / 100u);
+        wr(sm, L, (L.I + 1u) & 0xFFFu, (vx / 10u) % 10u);
+        wr(sm, L, (L.I + 2u) & 0xFFFu, vx % 10u);
+      } else {
+        if (f55) {
           for (uint32_t k = 0; k <= x; ++k) wr(sm, L, (L.I + k) & 0xFFFu, VREG(k));
-          if (p.quirks & 2u) L.I = (L.I + x + 1u) & 0xFFFFu;
-          break;
-        case 0x65:
+        } else {
           for (uint32_t k = 0; k <= x; ++k) VREG(k) = rd(sm, L, (L.I + k) & 0xFFFu);
-          if (p.quirks & 2u) L.I = (L.I + x + 1u) & 0xFFFFu;
-          break;
-        default: L.halted = 1; return;
+        }
+        if (p.quirks & 2u) L.I = (L.I + x + 1u) & 0xFFFFu;
       }
-      break;
     }
+  }
+  const bool do_draw = act & (hi == 0xDu);
+  if (__any_sync(kFull, do_draw)) {
+    const uint32_t y0 = vy & 31u;
+    const uint32_t nrows = do_draw ? (((p.quirks & 8u) != 0u) ? n : min(n, 32u - y0)) : 0u;
+    const uint32_t maxr = __reduce_max_sync(kFull, nrows);
+    if (maxr <= kLaneDrawMax)
+      draw_lanes(sm, L, p, tid, do_draw, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr);
+    else
+      draw_coop(sm, L, p, tid, lane, block0, do_draw, vx & 63u, y0, L.I & 0xFFFu, n);
+    __syncwarp();
   }
 }
 
-__device__ __forceinline__ void frame(Smem &sm, Lane &L, const StepParams &p, int tid, uint32_t gid) {
-  for (uint32_t k = 0; k < p.ipf; ++k) {
-    if (L.halted) break;
-    cycle(sm, L, p, tid, gid);
-  }
-  if (!L.halted) {
-    L.dt -= (L.dt != 0);
-    L.st -= (L.st != 0);
+// `frames` frames of ipf cycles + timer tick, for lanes with `part` (uniform loop counts)
+__device__ __forceinline__ void run_frames(Smem &sm, Lane &L, const StepParams &p, int tid, int lane, uint64_t block0,
+                                           uint32_t gid, bool part, uint32_t frames) {
+  for (uint32_t f = 0; f < frames; ++f) {
+    for (uint32_t k = 0; k < p.ipf; ++k) cycle(sm, L, p, tid, lane, block0, gid, part);
+    if (part && !L.halted) {
+      L.dt -= (L.dt != 0u);
+      L.st -= (L.st != 0u);
+    }
   }
 }
 
@@ -321,26 +452,26 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   const uint32_t h = p.head;
   uint64_t *__restrict__ ring = p.s.ring;
   uint64_t *__restrict__ obs64 = reinterpret_cast<uint64_t *>(obs);
+  const int ne = p.n > wbase ? (int)((p.n - wbase) < 32 ? (p.n - wbase) : 32) : 0;
 
   if (tid == 0) image_load_issue(sm, p.s.image);
 
-  // ---- warp-cooperative prologue: obs planes 0..2 <- ring, framebuffer <- ring[h]
+  // ---- prologue: framebuffer <- ring[h] with asynchronous 8-byte copies (LDGSTS),
+  //      lane = row, no register round trip; obs planes 0..2 are copied later,
+  //      pipelined behind the interpreter (see the frame loop).
+  const uint32_t s0 = (h + 2) & 3, s1 = (h + 3) & 3, s2 = h & 3;
   if (MODE == MODE_STEP) {
-    const uint32_t s0 = (h + 2) & 3, s1 = (h + 3) & 3, s2 = h & 3;
-    const int ne = p.n > wbase ? (int)((p.n - wbase) < 32 ? (p.n - wbase) : 32) : 0;
-#pragma unroll 4
     for (int e = 0; e < ne; ++e) {
-      const uint64_t *rg = ring + (wbase + e) * 128;
-      uint64_t r0 = rg[s0 * 32 + lane], r1 = rg[s1 * 32 + lane], r2 = rg[s2 * 32 + lane];
-      uint64_t *ob = obs64 + (wbase + e) * 128;
-      ob[lane] = r0;
-      ob[32 + lane] = r1;
-      ob[64 + lane] = r2;
-      sm.fb[(warp * 32 + e) * kFbStride + lane] = bswap64(r2);
+      const uint64_t *src = ring + (wbase + e) * 128 + s2 * 32 + lane;
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&sm.fb[fb_idx(warp * 32 + e, lane)]);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
 
   Lane L;
+  L.pc = 0x200; L.I = 0; L.sp = 0; L.dt = 0; L.st = 0; L.halted = 1; L.keys = 0; L.draw = 0; L.episode = 0;
+  L.dirty = 0; L.ram = p.s.ram; L.stk_dirty = 0;
   uint32_t steps = 0, prev = 0;
   int32_t ep_ret = 0;
   const uint32_t gid = (uint32_t)(p.env_offset + env);
@@ -361,79 +492,103 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     for (int k = 0; k < 16; ++k) sm.stk[k * kBlock + tid] = (uint16_t)(sw[k >> 1] >> (16 * (k & 1)));
     L.dirty = p.s.dirty[env];
     L.ram = p.s.ram + env * 4096ull;
-    L.keys = 0;
-    L.stk_dirty = 0;
   }
-  __syncthreads();  // mbarrier init visible
+  if (MODE == MODE_STEP) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  __syncthreads();  // mbarrier init + framebuffer rows visible
   image_load_wait(sm);
 
-  uint32_t did_reset = 0, err = 0, done = 0, term = 0, trunc = 0, finished = 0;
+  uint32_t done = 0, term = 0, trunc = 0, finished = 0, err = 0;
   float rew = 0.f;
   long long ret_acc = 0;
-  if (active) {
-    uint32_t frames_left, seg = 0;
-    bool resetting;
-    if (MODE == MODE_STEP) {
+  bool resetting;
+  if (MODE == MODE_STEP) {
+    // obs plane 2 = display at the start of the step (from smem, before any draw)
+    for (int e = 0; e < ne; ++e) obs64[(wbase + e) * 128 + 64 + lane] = sm.fb[fb_idx(warp * 32 + e, lane)];
+    if (active) {
       int32_t a = actions[env];
       if (a < 0 || (uint32_t)a >= p.n_actions) { err = 1; a = 0; }
       L.keys = p.keymask[a];
-      frames_left = p.frame_skip;
-      resetting = false;
-    } else {
-      L.episode = 0;
-      power_on(sm, L, tid);
-      frames_left = 0;
-      resetting = true;
     }
-    for (;;) {
-      for (; frames_left; --frames_left) frame(sm, L, p, tid, gid);
-      if (!resetting) {
-        uint32_t s = eval(p.score, sm, L, tid);
-        int32_t d = (int32_t)(s - prev);
-        rew = (float)d;
-        prev = s;
-        ep_ret = (int32_t)((uint32_t)ep_ret + (uint32_t)d);
-        steps++;
-        term = (eval(p.term, sm, L, tid) != 0u) || L.halted;
-        trunc = p.max_steps && steps >= p.max_steps;
-        done = term | trunc;
-        if (!done) break;
-        ret_acc = ep_ret;
-        finished = 1;
-        L.episode++;
-        power_on(sm, L, tid);
-        resetting = true;
-        did_reset = 1;
+    // frame loop; env `cur` of this warp gets its obs planes 0,1 copied per VM cycle:
+    // loads issued before the cycle, stores after it, so HBM latency hides behind it
+    int cur = 0;
+    for (uint32_t f = 0; f < p.frame_skip; ++f) {
+      for (uint32_t k = 0; k < p.ipf; ++k) {
+        const bool cp = cur < ne;
+        uint64_t q0 = 0, q1 = 0;
+        if (cp) {
+          const uint64_t *rg = ring + (wbase + cur) * 128;
+          q0 = __ldcs(rg + s0 * 32 + lane);
+          q1 = __ldcs(rg + s1 * 32 + lane);
+        }
+        cycle(sm, L, p, tid, lane, block0, gid, active);
+        if (cp) {
+          uint64_t *ob = obs64 + (wbase + cur) * 128;
+          __stcs(ob + lane, q0);
+          __stcs(ob + 32 + lane, q1);
+          ++cur;
+        }
       }
-      if (seg < p.n_startup) {
-        L.keys = p.startup_keys[seg];
-        frames_left = p.startup_frames[seg];
-        ++seg;
-        continue;
+      if (active && !L.halted) {
+        L.dt -= (L.dt != 0u);
+        L.st -= (L.st != 0u);
       }
-      L.keys = 0;
-      steps = 0;
-      prev = eval(p.score, sm, L, tid);
-      ep_ret = 0;
-      did_reset = 1;
-      break;
     }
-    if (MODE == MODE_STEP) {
+#pragma unroll 4
+    for (int e = cur; e < ne; ++e) {
+      const uint64_t *rg = ring + (wbase + e) * 128;
+      uint64_t *ob = obs64 + (wbase + e) * 128;
+      const uint64_t q0 = __ldcs(rg + s0 * 32 + lane), q1 = __ldcs(rg + s1 * 32 + lane);
+      __stcs(ob + lane, q0);
+      __stcs(ob + 32 + lane, q1);
+    }
+    if (active) {
+      const uint32_t s = eval(p.score, sm, L, tid);
+      const int32_t d = (int32_t)(s - prev);
+      rew = (float)d;
+      prev = s;
+      ep_ret = (int32_t)((uint32_t)ep_ret + (uint32_t)d);
+      steps++;
+      term = (eval(p.term, sm, L, tid) != 0u) || L.halted;
+      trunc = p.max_steps && steps >= p.max_steps;
+      done = term | trunc;
+      if (done) { ret_acc = ep_ret; finished = 1; L.episode++; }
       reward[env] = rew;
       done_out[env] = (uint8_t)done;
       if (term_out) term_out[env] = (uint8_t)term;
       if (trunc_out) trunc_out[env] = (uint8_t)trunc;
+    }
+    resetting = active && done;
+  } else {
+    resetting = active;
+    L.episode = 0;
+  }
+
+  // ---- same-step auto-reset: power-on + startup segments (warp-uniform)
+  const uint32_t reset_mask = __ballot_sync(kFull, resetting);
+  if (reset_mask) {
+    if (resetting) power_on(sm, L, tid);
+    __syncwarp();
+    for (uint32_t seg = 0; seg < p.n_startup; ++seg) {
+      if (resetting) L.keys = p.startup_keys[seg];
+      run_frames(sm, L, p, tid, lane, block0, gid, resetting, p.startup_frames[seg]);
+    }
+    if (resetting) {
+      L.keys = 0;
+      steps = 0;
+      prev = eval(p.score, sm, L, tid);
+      ep_ret = 0;
     }
   }
   __syncwarp();
 
   // ---- warp-cooperative epilogue: new ring slot + obs plane 3 (all planes on reset)
   {
-    const uint32_t reset_mask = __ballot_sync(0xffffffffu, did_reset);
     const uint32_t sn = (h + 1) & 3;
-    const int ne = p.n > wbase ? (int)((p.n - wbase) < 32 ? (p.n - wbase) : 32) : 0;
     for (int e = 0; e < ne; ++e) {
-      uint64_t v = bswap64(sm.fb[(warp * 32 + e) * kFbStride + lane]);
+      const uint64_t v = sm.fb[fb_idx(warp * 32 + e, lane)];
       uint64_t *rg = ring + (wbase + e) * 128;
       uint64_t *ob = obs64 ? obs64 + (wbase + e) * 128 : nullptr;
       if (MODE == MODE_STEP) {
@@ -477,10 +632,10 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     unsigned long long r = (unsigned long long)ret_acc, f = finished, st = active ? 1u : 0u, er = err;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-      r += __shfl_xor_sync(0xffffffffu, r, o);
-      f += __shfl_xor_sync(0xffffffffu, f, o);
-      st += __shfl_xor_sync(0xffffffffu, st, o);
-      er |= __shfl_xor_sync(0xffffffffu, er, o);
+      r += __shfl_xor_sync(kFull, r, o);
+      f += __shfl_xor_sync(kFull, f, o);
+      st += __shfl_xor_sync(kFull, st, o);
+      er |= __shfl_xor_sync(kFull, er, o);
     }
     if (lane == 0) { sm.red[0][warp] = r; sm.red[1][warp] = f; sm.red[2][warp] = st; sm.red[3][warp] = er; }
     __syncthreads();
