@@ -181,35 +181,67 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU arm
-def time_config(rom, spec, n, steps, warmup, rank_offset, aseed, torch, OctaxEnv, stream, barrier=None,
-                keep=False):
+def time_config(rom, spec, n, steps, warmup, rank_offset, aseed, torch, OctaxEnv, barrier=None,
+                keep=False, graph=False):
+    """Time `steps` octax_step launches (each = one step of all n envs) on a dedicated
+    stream with CUDA events; graph=True captures the K launches in one CUDA graph
+    (K % 4 == 0 keeps the 4-slot display ring aligned across replays)."""
+    stream = torch.cuda.Stream()
     env = OctaxEnv(rom, spec, n, 0x0C7A251001764000, env_offset=rank_offset, stream=stream)
     T = warmup + steps
     acts = torch.empty((T, n), dtype=torch.int32, device="cuda")
-    for t in range(T):
-        env.gen_actions(aseed, t, acts[t])
+    with torch.cuda.stream(stream):
+        for t in range(T):
+            env.gen_actions(aseed, t, acts[t])
     obs, rew, done = env.obs, env.reward, env.done
     for t in range(warmup):
         env.step_into(acts[t], obs, rew, done)
+    g = None
+    if graph:
+        assert steps % 4 == 0
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for k in range(steps):
+                env.step_into(acts[warmup + k], obs, rew, done)
+        with torch.cuda.stream(stream):
+            g.replay()  # warm replay
     torch.cuda.synchronize()
     if barrier:
         barrier()
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
     ev[0].record(stream)
-    for k in range(steps):
-        env.step_into(acts[warmup + k], obs, rew, done)
-        ev[k + 1].record(stream)
+    if graph:
+        with torch.cuda.stream(stream):
+            g.replay()
+        ev[steps].record(stream)
+    else:
+        for k in range(steps):
+            env.step_into(acts[warmup + k], obs, rew, done)
+            ev[k + 1].record(stream)
     torch.cuda.synchronize()
     if barrier:
         barrier()
-    per = [ev[k].elapsed_time(ev[k + 1]) for k in range(steps)]
+    per = [] if graph else [ev[k].elapsed_time(ev[k + 1]) for k in range(steps)]
     total_ms = ev[0].elapsed_time(ev[steps])
     if not keep:
-        del acts
+        del g, acts
         env.close()
         return total_ms, per, None
-    return total_ms, per, (env, acts)
+    return total_ms, per, (env, acts, stream)
+
+
+def issue_model(game, n):
+    """Warp instructions per env step measured by ncu (profiles/latest_step_full.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "latest_step_full.json")) as f:
+            j = json.load(f)
+        if j.get("game") == game:
+            return j
+    except Exception:
+        pass
+    return None
 
 
 def main():
@@ -236,7 +268,8 @@ def main():
     import workloads
     from paper_2510_01764_b200 import OctaxEnv
 
-    rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
+    from paper_2510_01764_b200 import dist as odist
+    rank, world, local = odist.rank_info()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -245,24 +278,21 @@ def main():
         if world > 1:
             dist.barrier()
 
-    stream = torch.cuda.current_stream()
     rom, spec = workloads.game(args.game)
     n = args.envs
-    offset = rank * n
+    offset, _ = odist.shard(rank, world, n)
 
     # ---- headline: n envs per GPU, K timed steps
     with ClockSampler(local) as clk:
         total_ms, per, kept = time_config(rom, spec, n, args.steps, args.warmup, offset,
-                                          workloads.ACTION_SEED, torch, OctaxEnv, stream, barrier, keep=True)
+                                          workloads.ACTION_SEED, torch, OctaxEnv, barrier, keep=True)
         # one NCCL all-reduce of the integer episode statistics per rollout
-        env, acts = kept
+        env, acts, stream = kept
         st = torch.zeros(4, dtype=torch.int64, device="cuda")
         env.stats_device(st)
-        if world > 1:
-            dist.all_reduce(st)
-    t_ms = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+        stream.synchronize()
+        odist.reduce_stats(st)
+    t_ms = odist.max_over_ranks(torch.tensor([total_ms], dtype=torch.float64, device="cuda"))
     t_max = float(t_ms.item())
     value = world * n * args.steps / (t_max / 1e3)
     kernel_ms = sorted(per)[len(per) // 2]
@@ -270,15 +300,25 @@ def main():
     hbm_peak, peak_src = _peaks()
     achieved = ALG_BYTES_PER_ENV_STEP * n / (kernel_ms / 1e3) / 1e9
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic_per_launch.json")
-    if os.path.exists(tp):
+    im_t = issue_model(args.game, n)
+    if im_t and im_t.get("envs") == n and im_t.get("dram_bytes_per_launch"):
+        traffic = im_t["dram_bytes_per_launch"]   # ncu --set full, same launch configuration
+
+    issue = None
+    im = issue_model(args.game, n)
+    if im and im.get("warp_instr_per_env_step"):
+        clk_mhz = None
         try:
-            with open(tp) as f:
-                tj = json.load(f)
-            if tj.get("envs") == n and tj.get("game") == args.game:
-                traffic = tj.get("dram_bytes_per_launch")
+            clk_mhz = clk.summary()["sm_mhz"]
         except Exception:
             pass
+        f_sm = (clk_mhz or 1965.0) * 1e6
+        peak_wi = 148 * 4 * f_sm  # warp instructions / s: 148 SMs x 4 schedulers x 1 issue/clk
+        wi = im["warp_instr_per_env_step"]
+        issue = {"warp_instr_per_env_step": wi, "source": im.get("source"),
+                 "peak_warp_instr_per_s": peak_wi, "roof_env_steps_per_s": peak_wi / wi,
+                 "frac": value / world / (peak_wi / wi),
+                 "warp_exec_efficiency": im.get("warp_exec_efficiency")}
 
     # ---- e2e through the host-buffer C-ABI call (H2D actions, D2H obs/reward/done)
     e2e = None
@@ -295,9 +335,7 @@ def main():
         t0 = time.perf_counter()
         for k in range(K):
             env.step_host(nd(a_h[k]), nd(o_h), nd(r_h), nd(d_h))
-        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        dt = odist.max_over_ranks(torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda"))
         e2e = {"value": world * n * K / float(dt.item()), "unit": "env steps/s",
                "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": (env.obs_per_env + 4 + 1) * n,
                "steps": K, "path": "octax_step_host (pinned host buffers)"}
@@ -305,22 +343,27 @@ def main():
     del acts
     torch.cuda.empty_cache()
 
-    # ---- sweep of smaller per-GPU env counts (context; parity-test configs)
+    # ---- sweep of smaller per-GPU env counts (context; parity-test configs): per-launch
+    #      and CUDA-graph-captured (launch overhead dominates below ~64K envs)
     sweep = []
     if not args.no_sweep:
+        ks = max(4, (args.steps // 4) * 4)
         for m in (1024, 4096, 65536, 262144):
             if m >= n:
                 continue
-            tm, pm, _ = time_config(rom, spec, m, args.steps, args.warmup, rank * m,
-                                    workloads.ACTION_SEED, torch, OctaxEnv, stream, barrier)
-            tt = torch.tensor([tm], dtype=torch.float64, device="cuda")
-            if world > 1:
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            sps = world * m * args.steps / (float(tt.item()) / 1e3)
-            sweep.append({"envs_per_gpu": m, "steps_per_s": sps, "frames_per_s": 4 * sps,
-                          "ms_per_step": float(tt.item()) / args.steps})
-        sweep.append({"envs_per_gpu": n, "steps_per_s": value, "frames_per_s": 4 * value,
-                      "ms_per_step": t_max / args.steps})
+            row = {"envs_per_gpu": m}
+            for graph in (False, True):
+                tm, _, _ = time_config(rom, spec, m, ks, args.warmup, odist.shard(rank, world, m)[0],
+                                       workloads.ACTION_SEED, torch, OctaxEnv, barrier, graph=graph)
+                tt = float(odist.max_over_ranks(torch.tensor([tm], dtype=torch.float64, device="cuda")).item())
+                sps = world * m * ks / (tt / 1e3)
+                key = "graph" if graph else "launch"
+                row[f"steps_per_s_{key}"] = sps
+                row[f"ms_per_step_{key}"] = tt / ks
+            row["frames_per_s_graph"] = 4 * row["steps_per_s_graph"]
+            sweep.append(row)
+        sweep.append({"envs_per_gpu": n, "steps_per_s_launch": value, "frames_per_s_launch": 4 * value,
+                      "ms_per_step_launch": t_max / args.steps})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -346,7 +389,9 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
                          "kernel": "octax_kernel<MODE_STEP>", "kernel_ms_median": kernel_ms,
-                         "alg_bytes_per_env_step": ALG_BYTES_PER_ENV_STEP, "peak_source": peak_src},
+                         "alg_bytes_per_env_step": ALG_BYTES_PER_ENV_STEP, "peak_source": peak_src,
+                         "hbm_roof_env_steps_per_s": hbm_peak * 1e9 / ALG_BYTES_PER_ENV_STEP,
+                         "issue": issue},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps,

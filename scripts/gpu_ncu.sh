@@ -3,7 +3,7 @@
 cd "$GRAFT_REPO_ROOT"
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
-ENVS=${ENVS:-262144}
+ENVS=${ENVS:-1048576}
 TAG=${TAG:-prof}
 PCMD="python bench.py --steps 3 --warmup 3 --envs $ENVS --no-sweep --no-e2e --no-cpu"
 timeout 300 $PCMD > gpurun_out/plain_prof.log 2>&1 && \

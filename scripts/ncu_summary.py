@@ -83,6 +83,15 @@ def full(path, out, extra):
             js["dram_bytes_per_launch"] = rb + wb
         except Exception:
             pass
+    if res and "envs" in extra:
+        try:
+            r0 = res[0]
+            js["warp_instr_per_env_step"] = float(r0["smsp__inst_executed.sum"]["value"]) / extra["envs"]
+            js["warp_exec_efficiency"] = float(r0["smsp__thread_inst_executed_per_inst_executed.ratio"]["value"]) / 32
+            if "dram_bytes_per_launch" in js:
+                js["dram_bytes_per_env_step"] = js["dram_bytes_per_launch"] / extra["envs"]
+        except Exception:
+            pass
     with open(out, "w") as f:
         json.dump(js, f, indent=1)
     for d in res:
