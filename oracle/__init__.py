@@ -86,6 +86,7 @@ def lib():
                                                     ctypes.c_uint64, ctypes.c_uint32]
         L.octax_oracle_synthetic_action.restype = ctypes.c_int32
         L.octax_oracle_counters.argtypes = [P, ctypes.c_uint64, P]
+        L.octax_oracle_tick_timers.argtypes = [P, ctypes.c_uint64]
         _lib = L
     return _lib
 
@@ -192,6 +193,9 @@ class OracleEnv:
 
     def run_frames(self, env: int, n: int, keys: int = 0) -> None:
         _check(lib().octax_oracle_run_frames(self._h, env, n, keys))
+
+    def tick_timers(self, env: int) -> None:
+        _check(lib().octax_oracle_tick_timers(self._h, env))
 
     def counters(self, env: int) -> np.ndarray:
         out = np.zeros(17, np.uint64)

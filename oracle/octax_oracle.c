@@ -933,6 +933,16 @@ int octax_oracle_run_frames(oracle_env *e, uint64_t env, uint32_t n, uint16_t ke
   return ORACLE_OK;
 }
 
+int octax_oracle_tick_timers(oracle_env *e, uint64_t env) {
+  if (!e || env >= e->n) return fail(ORACLE_E_INVALID_ARG, "bad env");
+  vm *m = &e->vms[env];
+  if (!m->halted) {
+    if (m->DT > 0) m->DT--;
+    if (m->ST > 0) m->ST--;
+  }
+  return ORACLE_OK;
+}
+
 int octax_oracle_eval_expr(const char *expr, const uint8_t *canon_state,
                            uint32_t *value_out, size_t *err_offset_out) {
   if (!expr) return fail(ORACLE_E_INVALID_ARG, "expr is NULL");

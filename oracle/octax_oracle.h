@@ -93,6 +93,8 @@ const char *octax_oracle_last_error(void);
 int octax_oracle_run_cycles(oracle_env *e, uint64_t env, uint32_t n, uint16_t keys);
 /* Run n frames (ipf cycles, then the timer tick) with `keys` held. */
 int octax_oracle_run_frames(oracle_env *e, uint64_t env, uint32_t n, uint16_t keys);
+/* The 60 Hz timer tick of one frame alone, for cycle-level tracing. */
+int octax_oracle_tick_timers(oracle_env *e, uint64_t env);
 /* Parse + evaluate an expression against a canonical state. */
 int octax_oracle_eval_expr(const char *expr, const uint8_t *canon_state,
                            uint32_t *value_out, size_t *err_offset_out);

@@ -38,9 +38,8 @@ constexpr uint32_t kLaneDrawMax = 8;  // rows: lane-parallel DXYN up to this, co
 struct __align__(128) Smem {
   uint8_t img[kImageBytes];                  // pristine image (TMA destination)
   uint64_t fb[kBlock * 32];                  // framebuffer rows, bit 63-x = pixel x, swizzled
-  uint32_t V[16 * kBlock];                   // V[k*kBlock + tid]
+  uint8_t V[16 * kBlock];                    // V[k] of env t at k*128 + (t ^ 4k): bank (t>>2)^k
   uint16_t stk[16 * kBlock];                 // stk[k*kBlock + tid]
-  uint32_t evs[kMaxDepth * kBlock];          // expression stack (below top)
   uint32_t dprm[kBlock / 32][32];            // DXYN owner params (x0 | y0 << 6 | base << 11)
   uint8_t down[kBlock / 32][32];             // DXYN item -> owner lane map
   unsigned long long red[4][kBlock / 32];    // per-warp statistics
@@ -106,7 +105,7 @@ struct Lane {
   uint32_t stk_dirty;
 };
 
-#define VREG(k) sm.V[(k)*kBlock + tid]
+#define VREG(k) sm.V[((k) << 7) + ((uint32_t)tid ^ ((uint32_t)(k) << 2))]
 
 __device__ __forceinline__ uint32_t rd(const Smem &sm, const Lane &L, uint32_t a) {
   return ((L.dirty >> (a >> 6)) & 1ull) ? (uint32_t)L.ram[a] : (uint32_t)sm.img[a];
@@ -193,7 +192,7 @@ __device__ __forceinline__ void draw_coop(Smem &sm, const Lane &L, const StepPar
     hitmask |= __reduce_or_sync(kFull, hit ? (1u << j) : 0u);
     __syncwarp();
   }
-  if (do_draw) VREG(15) = (hitmask >> lane) & 1u;
+  if (do_draw) VREG(15) = (uint8_t)((hitmask >> lane) & 1u);
 }
 
 // DXYN, lane-parallel: every drawing lane XORs its own rows, loop bound = the
@@ -203,14 +202,32 @@ __device__ __forceinline__ void draw_coop(Smem &sm, const Lane &L, const StepPar
 // The framebuffer holds rows in packed byte order (byte b = pixels 8b..8b+7, MSB
 // leftmost), so the mask is built as bswap16(sprite << 8 >> (x0 & 7)) << 8*(x0 >> 3).
 __device__ __forceinline__ void draw_lanes(Smem &sm, Lane &L, const StepParams &p, int tid, bool do_draw,
-                                           uint32_t x0, uint32_t y0, uint32_t base, uint32_t nrows, uint32_t maxr) {
-  const bool wrap = (p.quirks & 8u) != 0;
-  const bool slowb = do_draw & ((((L.dirty >> (base >> 6)) & 3ull) != 0ull) | (base + 15u > 0xFFFu));
+                                           uint32_t x0, uint32_t y0, uint32_t base, uint32_t nrows, uint32_t maxr,
+                                           bool wdirty, uint32_t quirks) {
+  const bool wrap = (quirks & 8u) != 0;
+  bool slowb = do_draw & (base + 15u > 0xFFFu);
+  if (wdirty) slowb |= do_draw & (((L.dirty >> (base >> 6)) & 3ull) != 0ull);
   const uint32_t sh = x0 & 7u, q8 = (x0 >> 3) * 8u, swz = (uint32_t)tid & 15u;
   uint64_t *rows = &sm.fb[(uint32_t)tid * 32u];
-  const uint8_t *spr = sm.img + (base & 0xFFFu);
   uint64_t hit = 0;
-  if (__any_sync(kFull, slowb)) {
+  if (!wrap && !__any_sync(kFull, slowb)) {
+    // sprite bytes base..base+7 realigned from three 32-bit image words
+    const uint32_t *w = reinterpret_cast<const uint32_t *>(sm.img + (base & 0xFFCu));
+    const uint32_t off8 = (base & 3u) * 8u, w0 = w[0], w1 = w[1], w2 = w[2];
+    const uint32_t v0 = __funnelshift_r(w0, w1, off8), v1 = __funnelshift_r(w1, w2, off8);
+    const uint32_t sl = 8u - sh;
+#pragma unroll
+    for (uint32_t r = 0; r < kLaneDrawMax; ++r) {
+      if (r >= maxr) break;
+      uint32_t byte = ((r < 4 ? v0 : v1) >> (8u * (r & 3u))) & 255u;
+      byte = r < nrows ? byte : 0u;
+      const uint64_t m = (uint64_t)__byte_perm(byte << sl, 0, 0x4401) << q8;
+      uint64_t *row = rows + (((y0 + r) & 31u) ^ swz);
+      const uint64_t old = *row;
+      *row = old ^ m;
+      hit |= old & m;
+    }
+  } else {
     for (uint32_t r = 0; r < maxr; ++r) {
       const uint32_t a = base + r;
       uint32_t byte = (r < nrows && a <= 0xFFFu) ? rd(sm, L, a) : 0u;
@@ -221,40 +238,24 @@ __device__ __forceinline__ void draw_lanes(Smem &sm, Lane &L, const StepParams &
       *row = old ^ m;
       hit |= old & m;
     }
-  } else if (!wrap) {
-    for (uint32_t r = 0; r < maxr; ++r) {
-      const uint32_t byte = r < nrows ? (uint32_t)spr[r] : 0u;
-      const uint64_t m = (uint64_t)__byte_perm((byte << 8) >> sh, 0, 0x4401) << q8;
-      uint64_t *row = rows + (((y0 + r) & 31u) ^ swz);
-      const uint64_t old = *row;
-      *row = old ^ m;
-      hit |= old & m;
-    }
-  } else {
-    for (uint32_t r = 0; r < maxr; ++r) {
-      const uint32_t byte = r < nrows ? (uint32_t)spr[r] : 0u;
-      const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> sh, 0, 0x4401);
-      const uint64_t m = (w << q8) | (q8 ? (w >> (64u - q8)) : 0ull);
-      uint64_t *row = rows + (((y0 + r) & 31u) ^ swz);
-      const uint64_t old = *row;
-      *row = old ^ m;
-      hit |= old & m;
-    }
   }
-  if (do_draw) VREG(15) = hit != 0ull;
+  if (do_draw) VREG(15) = (uint8_t)(hit != 0ull);
 }
 
 // One CHIP-8 cycle for every lane with `part` (must be called by all 32 lanes).
 // Branch-free predicated core; class tests are one-hot masks cm = 1 << (op >> 12).
+template <bool Q0>
 __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, int tid, int lane, uint64_t block0,
-                                      uint32_t gid, bool part) {
+                                      uint32_t gid, bool part, bool &wdirty) {
+  const uint32_t quirks = Q0 ? 0u : p.quirks;  // Q0: modern profile specialisation
   bool act = part & (L.halted == 0u);
   const uint32_t pc = L.pc;
   const bool oob = pc > 0xFFEu;
   // ---- fetch: one 8-byte load from the smem image (slow path: dirty block or straddle)
   const uint64_t w8 = *reinterpret_cast<const uint64_t *>(sm.img + (pc & 0xFF8u));
   uint32_t op = __byte_perm((uint32_t)(w8 >> ((pc & 7u) * 8u)), 0, 0x4401);
-  const bool slow = act & !oob & (((pc & 7u) == 7u) | (((L.dirty >> (pc >> 6)) & 1ull) != 0ull));
+  bool slow = act & !oob & ((pc & 7u) == 7u);
+  if (wdirty) slow |= act & !oob & (((L.dirty >> (pc >> 6)) & 1ull) != 0ull);
   if (__any_sync(kFull, slow)) {
     if (slow) op = (rd(sm, L, pc) << 8) | rd(sm, L, pc + 1);
   }
@@ -288,7 +289,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   const bool skip = (((cm & 0x0028u) != 0u) & eq) | (((cm & 0x0210u) != 0u) & !eq) |
                     ((hi == 0xEu) & (keyd ^ (nn == 0xA1u)));
   // ---- ALU 8XYn; flag written after the result (A15)
-  const uint32_t s = (p.quirks & 1u) ? vy : vx;
+  const uint32_t s = (quirks & 1u) ? vy : vx;
   const bool sub5 = n == 5u, sub7 = n == 7u;
   const uint32_t sa = sub7 ? vy : vx;
   uint32_t sb = vy;
@@ -307,7 +308,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   r8 = (n == 0xEu) ? ((s << 1) & 255u) : r8;
   f8 = (n == 0xEu) ? (s >> 7) : f8;
   const bool is8 = hi == 8u;
-  const bool wvf = act & is8 & ((n >= 4u) | (((p.quirks & 16u) != 0u) & (n >= 1u)));
+  const bool wvf = act & is8 & ((n >= 4u) | (((quirks & 16u) != 0u) & (n >= 1u)));
   // ---- register writes
   uint32_t nvx = nn;
   nvx = (hi == 7u) ? ((vx + nn) & 255u) : nvx;
@@ -315,14 +316,14 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   nvx = f07 ? L.dt : nvx;
   nvx = f0a ? (uint32_t)(__ffs(L.keys) - 1) : nvx;
   const bool wvx = act & (((cm & 0x01C0u) != 0u) | f07 | (f0a & (L.keys != 0u)));
-  if (wvx) VREG(x) = nvx;
-  if (wvf) VREG(15) = f8;
+  if (wvx) VREG(x) = (uint8_t)nvx;
+  if (wvf) VREG(15) = (uint8_t)f8;
   // ---- control flow and index / timer registers
   uint32_t npc = pc + (skip ? 4u : 2u);
   npc = ((cm & 0x0006u) != 0u) ? nnn : npc;  // 1NNN, 2NNN
   npc = is_ret ? ret_pc : npc;
   npc = (f0a & (L.keys == 0u)) ? pc : npc;   // A16: FX0A re-executes while no key
-  if (act & (hi == 0xBu)) npc = (nnn + VREG((p.quirks & 4u) ? x : 0u)) & 0xFFFu;
+  if (act & (hi == 0xBu)) npc = (nnn + VREG((quirks & 4u) ? x : 0u)) & 0xFFFu;
   uint32_t I2 = L.I;
   I2 = (hi == 0xAu) ? nnn : I2;
   I2 = f1e ? ((I2 + vx) & 0xFFFFu) : I2;
@@ -346,7 +347,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   if (__any_sync(kFull, do_rnd)) {
     if (do_rnd) {
       const uint32_t r = philox_out0(L.draw, L.episode, gid, 0u, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
-      VREG(x) = r & nn & 255u;
+      VREG(x) = (uint8_t)(r & nn);
       L.draw++;
     }
   }
@@ -361,19 +362,20 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
         if (f55) {
           for (uint32_t k = 0; k <= x; ++k) wr(sm, L, (L.I + k) & 0xFFFu, VREG(k));
         } else {
-          for (uint32_t k = 0; k <= x; ++k) VREG(k) = rd(sm, L, (L.I + k) & 0xFFFu);
+          for (uint32_t k = 0; k <= x; ++k) VREG(k) = (uint8_t)rd(sm, L, (L.I + k) & 0xFFFu);
         }
-        if (p.quirks & 2u) L.I = (L.I + x + 1u) & 0xFFFFu;
+        if (quirks & 2u) L.I = (L.I + x + 1u) & 0xFFFFu;
       }
     }
+    wdirty = __any_sync(kFull, L.dirty != 0ull);
   }
   const bool do_draw = act & (hi == 0xDu);
   if (__any_sync(kFull, do_draw)) {
     const uint32_t y0 = vy & 31u;
-    const uint32_t nrows = do_draw ? (((p.quirks & 8u) != 0u) ? n : min(n, 32u - y0)) : 0u;
+    const uint32_t nrows = do_draw ? (((quirks & 8u) != 0u) ? n : min(n, 32u - y0)) : 0u;
     const uint32_t maxr = __reduce_max_sync(kFull, nrows);
     if (maxr <= kLaneDrawMax)
-      draw_lanes(sm, L, p, tid, do_draw, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr);
+      draw_lanes(sm, L, p, tid, do_draw, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks);
     else
       draw_coop(sm, L, p, tid, lane, block0, do_draw, vx & 63u, y0, L.I & 0xFFFu, n);
     __syncwarp();
@@ -381,10 +383,11 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
 }
 
 // `frames` frames of ipf cycles + timer tick, for lanes with `part` (uniform loop counts)
+template <bool Q0>
 __device__ __forceinline__ void run_frames(Smem &sm, Lane &L, const StepParams &p, int tid, int lane, uint64_t block0,
-                                           uint32_t gid, bool part, uint32_t frames) {
+                                           uint32_t gid, bool part, uint32_t frames, bool &wdirty) {
   for (uint32_t f = 0; f < frames; ++f) {
-    for (uint32_t k = 0; k < p.ipf; ++k) cycle(sm, L, p, tid, lane, block0, gid, part);
+    for (uint32_t k = 0; k < p.ipf; ++k) cycle<Q0>(sm, L, p, tid, lane, block0, gid, part, wdirty);
     if (part && !L.halted) {
       L.dt -= (L.dt != 0u);
       L.st -= (L.st != 0u);
@@ -392,53 +395,61 @@ __device__ __forceinline__ void run_frames(Smem &sm, Lane &L, const StepParams &
   }
 }
 
+// Postfix bytecode evaluator (uniform control flow: every lane runs the same
+// program).  The stack lives in registers as a shift register with compile-time
+// slots (depth <= kMaxDepth is enforced at create), so it costs no shared memory.
 __device__ __forceinline__ uint32_t eval(const Program &P, Smem &sm, const Lane &L, int tid) {
-  uint32_t tos = 0, sp = 0;
+  uint32_t st[kMaxDepth];
+#pragma unroll
+  for (int k = 0; k < kMaxDepth; ++k) st[k] = 0;
   for (uint32_t i = 0; i < P.len; ++i) {
     const ExprInsn in = P.ops[i];
-    uint32_t a = 0, b = tos;
-    if (in.op >= X_MUL) { --sp; a = sm.evs[sp * kBlock + tid]; }
-    switch (in.op) {
-      case X_CONST: case X_V: case X_I: case X_DT: case X_ST: {
-        uint32_t v = in.op == X_CONST ? in.imm
-                   : in.op == X_V   ? VREG(in.arg)
-                   : in.op == X_I   ? L.I
-                   : in.op == X_DT  ? L.dt : L.st;
-        sm.evs[sp * kBlock + tid] = tos;
-        ++sp;
-        tos = v;
-        break;
+    if (in.op <= X_ST) {  // push
+      const uint32_t v = in.op == X_CONST ? in.imm
+                       : in.op == X_V   ? (uint32_t)VREG(in.arg)
+                       : in.op == X_I   ? L.I
+                       : in.op == X_DT  ? L.dt : L.st;
+#pragma unroll
+      for (int k = kMaxDepth - 1; k > 0; --k) st[k] = st[k - 1];
+      st[0] = v;
+    } else if (in.op < X_MUL) {  // unary on the top
+      const uint32_t t = st[0];
+      st[0] = in.op == X_MEM ? rd(sm, L, t & 0xFFFu) : in.op == X_NEG ? 0u - t : in.op == X_NOT ? (uint32_t)(t == 0u) : ~t;
+    } else {  // binary: a = second, b = top
+      const uint32_t a = st[1], b = st[0];
+      uint32_t r;
+      switch (in.op) {
+        case X_MUL: r = a * b; break;
+        case X_DIV: r = b ? a / b : 0u; break;
+        case X_MOD: r = b ? a % b : 0u; break;
+        case X_ADD: r = a + b; break;
+        case X_SUB: r = a - b; break;
+        case X_SHL: r = b >= 32u ? 0u : a << b; break;
+        case X_SHR: r = b >= 32u ? 0u : a >> b; break;
+        case X_LT: r = a < b; break;
+        case X_LE: r = a <= b; break;
+        case X_GT: r = a > b; break;
+        case X_GE: r = a >= b; break;
+        case X_EQ: r = a == b; break;
+        case X_NE: r = a != b; break;
+        case X_AND: r = a & b; break;
+        case X_XOR: r = a ^ b; break;
+        case X_OR: r = a | b; break;
+        case X_LAND: r = (a != 0u) & (b != 0u); break;
+        default: r = (a != 0u) | (b != 0u); break;  // X_LOR
       }
-      case X_MEM: tos = rd(sm, L, tos & 0xFFFu); break;
-      case X_NEG: tos = 0u - tos; break;
-      case X_NOT: tos = tos == 0u; break;
-      case X_BNOT: tos = ~tos; break;
-      case X_MUL: tos = a * b; break;
-      case X_DIV: tos = b ? a / b : 0u; break;
-      case X_MOD: tos = b ? a % b : 0u; break;
-      case X_ADD: tos = a + b; break;
-      case X_SUB: tos = a - b; break;
-      case X_SHL: tos = b >= 32u ? 0u : a << b; break;
-      case X_SHR: tos = b >= 32u ? 0u : a >> b; break;
-      case X_LT: tos = a < b; break;
-      case X_LE: tos = a <= b; break;
-      case X_GT: tos = a > b; break;
-      case X_GE: tos = a >= b; break;
-      case X_EQ: tos = a == b; break;
-      case X_NE: tos = a != b; break;
-      case X_AND: tos = a & b; break;
-      case X_XOR: tos = a ^ b; break;
-      case X_OR: tos = a | b; break;
-      case X_LAND: tos = (a != 0u) & (b != 0u); break;
-      default: tos = (a != 0u) | (b != 0u); break;  // X_LOR
+#pragma unroll
+      for (int k = 1; k < kMaxDepth - 1; ++k) st[k] = st[k + 1];
+      st[kMaxDepth - 1] = 0;
+      st[0] = r;
     }
   }
-  return tos;
+  return st[0];
 }
 
 // ---------------------------------------------------------------- the step kernel
-template <int MODE>
-__global__ void __launch_bounds__(kBlock, 4)
+template <int MODE, bool Q0>
+__global__ void __launch_bounds__(kBlock, 5)
 octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ actions,
              uint8_t *__restrict__ obs, float *__restrict__ reward, uint8_t *__restrict__ done_out,
              uint8_t *__restrict__ term_out, uint8_t *__restrict__ trunc_out) {
@@ -479,7 +490,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     uint4 v = p.s.regs[env];
     uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int k = 0; k < 16; ++k) VREG(k) = (w[k >> 2] >> (8 * (k & 3))) & 255u;
+    for (int k = 0; k < 16; ++k) VREG(k) = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
     uint4 c = p.s.ctrl[env];
     L.pc = c.x & 0xFFFFu; L.I = c.x >> 16;
     L.sp = c.y & 255u; L.dt = (c.y >> 8) & 255u; L.st = (c.y >> 16) & 255u; L.halted = c.y >> 24;
@@ -498,6 +509,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   }
   __syncthreads();  // mbarrier init + framebuffer rows visible
   image_load_wait(sm);
+  bool wdirty = __any_sync(kFull, L.dirty != 0ull);  // any lane with private RAM blocks
 
   uint32_t done = 0, term = 0, trunc = 0, finished = 0, err = 0;
   float rew = 0.f;
@@ -523,7 +535,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
           q0 = __ldcs(rg + s0 * 32 + lane);
           q1 = __ldcs(rg + s1 * 32 + lane);
         }
-        cycle(sm, L, p, tid, lane, block0, gid, active);
+        cycle<Q0>(sm, L, p, tid, lane, block0, gid, active, wdirty);
         if (cp) {
           uint64_t *ob = obs64 + (wbase + cur) * 128;
           __stcs(ob + lane, q0);
@@ -573,7 +585,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     __syncwarp();
     for (uint32_t seg = 0; seg < p.n_startup; ++seg) {
       if (resetting) L.keys = p.startup_keys[seg];
-      run_frames(sm, L, p, tid, lane, block0, gid, resetting, p.startup_frames[seg]);
+      run_frames<Q0>(sm, L, p, tid, lane, block0, gid, resetting, p.startup_frames[seg], wdirty);
     }
     if (resetting) {
       L.keys = 0;
@@ -611,7 +623,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   if (active) {
     uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int k = 0; k < 16; ++k) w[k >> 2] |= (VREG(k) & 255u) << (8 * (k & 3));
+    for (int k = 0; k < 16; ++k) w[k >> 2] |= (uint32_t)VREG(k) << (8 * (k & 3));
     p.s.regs[env] = make_uint4(w[0], w[1], w[2], w[3]);
     p.s.ctrl[env] = make_uint4(L.pc | (L.I << 16), L.sp | (L.dt << 8) | (L.st << 16) | (L.halted << 24),
                                L.draw, L.episode);
@@ -747,30 +759,29 @@ __global__ void set_state_kernel(StepParams p, uint64_t env, const uint8_t *__re
 }
 
 // ---------------------------------------------------------------- launchers
-static bool g_attr_set[2] = {false, false};
+template <int MODE, bool Q0>
+static cudaError_t launch_variant(const StepParams &p, const int32_t *actions, uint8_t *obs, float *reward,
+                                  uint8_t *done, uint8_t *term, uint8_t *trunc, cudaStream_t stream) {
+  static bool attr_set = false;  // per template instance
+  const size_t smem = sizeof(Smem);
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(octax_kernel<MODE, Q0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const unsigned grid = (unsigned)((p.n + kBlock - 1) / kBlock);
+  octax_kernel<MODE, Q0><<<grid, kBlock, smem, stream>>>(p, actions, obs, reward, done, term, trunc);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_step(const StepParams &p, int mode, const int32_t *actions, uint8_t *obs, float *reward,
                         uint8_t *done, uint8_t *term, uint8_t *trunc, cudaStream_t stream) {
-  const size_t smem = sizeof(Smem);
-  const unsigned grid = (unsigned)((p.n + kBlock - 1) / kBlock);
-  if (mode == MODE_STEP) {
-    if (!g_attr_set[0]) {
-      cudaError_t e = cudaFuncSetAttribute(octax_kernel<MODE_STEP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-      g_attr_set[0] = true;
-    }
-    octax_kernel<MODE_STEP><<<grid, kBlock, smem, stream>>>(p, actions, obs, reward, done, term, trunc);
-  } else {
-    if (!g_attr_set[1]) {
-      cudaError_t e = cudaFuncSetAttribute(octax_kernel<MODE_RESET>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-      g_attr_set[1] = true;
-    }
-    octax_kernel<MODE_RESET><<<grid, kBlock, smem, stream>>>(p, nullptr, obs, nullptr, nullptr, nullptr, nullptr);
-  }
-  return cudaGetLastError();
+  const bool q0 = p.quirks == 0u;
+  if (mode == MODE_STEP)
+    return q0 ? launch_variant<MODE_STEP, true>(p, actions, obs, reward, done, term, trunc, stream)
+              : launch_variant<MODE_STEP, false>(p, actions, obs, reward, done, term, trunc, stream);
+  return q0 ? launch_variant<MODE_RESET, true>(p, nullptr, obs, nullptr, nullptr, nullptr, nullptr, stream)
+            : launch_variant<MODE_RESET, false>(p, nullptr, obs, nullptr, nullptr, nullptr, nullptr, stream);
 }
 
 cudaError_t launch_gen_actions(uint64_t n, uint64_t env_offset, uint64_t aseed, uint64_t t, uint32_t n_actions,
