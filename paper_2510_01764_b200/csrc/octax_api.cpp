@@ -298,6 +298,44 @@ octax_status compile_expr(const char *src, const char *what, Program &prog) {
   return OCTAX_OK;
 }
 
+// Decode table for the kernel core (see octax_dev.cuh).  Built from the ISA
+// definition (S:158 opcode list; readings A14/A20) with the quirk bits
+// folded in.
+void build_desc_table(uint32_t quirks, uint32_t out[kDescEntries]) {
+  for (uint32_t k = 0; k < kDescEntries; ++k) out[k] = 0;
+  for (uint32_t hi = 0; hi < 14; ++hi)
+    for (uint32_t n = 0; n < 16; ++n) {
+      uint32_t d = 0;
+      switch (hi) {
+        case 0x0: d = D_OK; break;  // 00E0 / 00EE / 0NNN decided from the full word
+        case 0x1: d = D_OK | D_PCJ; break;
+        case 0x2: d = D_OK | D_PCJ | D_CALL; break;
+        case 0x3: d = D_OK | D_SKIPEQ; break;
+        case 0x4: d = D_OK | D_SKIPNE; break;
+        case 0x5: d = n == 0 ? (D_OK | D_SKIPEQ | D_BVY) : 0u; break;
+        case 0x6: d = D_OK | D_WVX; break;
+        case 0x7: d = D_OK | D_WVX | D_VSADD; break;
+        case 0x8:
+          if (n <= 7 || n == 0xE) {
+            d = D_OK | D_WVX | D_VSALU;
+            if (n >= 4 || ((quirks & OCTAX_Q_VF_RESET) && n >= 1)) d |= D_WVF;
+          }
+          break;
+        case 0x9: d = n == 0 ? (D_OK | D_SKIPNE | D_BVY) : 0u; break;
+        case 0xA: d = D_OK | D_INNN; break;
+        case 0xB: d = D_OK | D_BJMP; break;
+        case 0xC: d = D_OK | D_RND; break;
+        case 0xD: d = D_OK | D_DRAW; break;
+      }
+      out[(hi << 4) | n] = d;
+    }
+  struct { uint32_t op; uint32_t d; } ef[] = {
+      {0xE09E, D_SKIPKEY}, {0xE0A1, D_SKIPNKEY}, {0xF007, D_WVX | D_VSDT}, {0xF00A, D_WAIT},
+      {0xF015, D_DTW},     {0xF018, D_STW},      {0xF01E, D_IADD},        {0xF029, D_IFONT},
+      {0xF033, D_MEM},     {0xF055, D_MEM},      {0xF065, D_MEM}};
+  for (auto &e : ef) out[desc_index(e.op)] = D_OK | D_NNCHK | e.d | ((e.op & 0xFFu) << 24);
+}
+
 // Canonical CHIP-8 font, 16 glyphs x 5 rows, stored at 0x050 (A23).
 const uint8_t kFont[80] = {
     0xF0, 0x90, 0x90, 0x90, 0xF0, 0x20, 0x60, 0x20, 0x20, 0x70, 0xF0, 0x10, 0xF0, 0x80, 0xF0, 0xF0,
@@ -413,7 +451,7 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   const uint64_t n = n_envs;
   size_t off = 0;
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
-  size_t o_img = carve(4096), o_stats = carve(64), o_regs = carve(16 * n), o_ctrl = carve(16 * n),
+  size_t o_img = carve(kStageBytes), o_stats = carve(64), o_regs = carve(16 * n), o_ctrl = carve(16 * n),
          o_book = carve(16 * n), o_stack = carve(32 * n), o_dirty = carve(8 * n), o_ring = carve(1024 * n),
          o_ram = carve(4096 * n);
   e->block_bytes = off;
@@ -432,11 +470,12 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   // state is fully written by the reset kernel; zero the small fields anyway
   ce = cudaMemsetAsync(base, 0, o_ring, e->stream);
   if (ce != cudaSuccess) { free_env(e); return cuda_err(ce, "cudaMemset"); }
-  uint8_t image[4096];
+  uint8_t image[kStageBytes];
   memset(image, 0, sizeof image);
   memcpy(image + 0x50, kFont, sizeof kFont);
   memcpy(image + 0x200, rom, rom_len);
-  ce = cudaMemcpyAsync(base + o_img, image, 4096, cudaMemcpyHostToDevice, e->stream);
+  build_desc_table(spec->quirks, reinterpret_cast<uint32_t *>(image + kImageBytes));
+  ce = cudaMemcpyAsync(base + o_img, image, kStageBytes, cudaMemcpyHostToDevice, e->stream);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->stream);
   if (ce != cudaSuccess) { free_env(e); return cuda_err(ce, "upload image"); }
   if (e->obs_format != OCTAX_OBS_PACKED) {

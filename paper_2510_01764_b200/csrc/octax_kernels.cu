@@ -36,7 +36,8 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr uint32_t kLaneDrawMax = 8;  // rows: lane-parallel DXYN up to this, cooperative above
 
 struct __align__(128) Smem {
-  uint8_t img[kImageBytes];                  // pristine image (TMA destination)
+  uint8_t img[kImageBytes];                  // pristine image (TMA destination) ...
+  uint32_t dtab[kDescEntries];               // ... immediately followed by the decode table
   uint64_t fb[kBlock * 32];                  // framebuffer rows, bit 63-x = pixel x, swizzled
   uint8_t V[16 * kBlock];                    // V[k] of env t at k*128 + (t ^ 4k): bank (t>>2)^k
   uint16_t stk[16 * kBlock];                 // stk[k*kBlock + tid]
@@ -77,11 +78,11 @@ __device__ __forceinline__ void image_load_issue(Smem &sm, const uint8_t *src) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kImageBytes)
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kStageBytes)
                : "memory");
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-      "l"(src), "r"(kImageBytes), "r"(bar)
+      "l"(src), "r"(kStageBytes), "r"(bar)
       : "memory");
 }
 
@@ -259,36 +260,28 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   if (__any_sync(kFull, slow)) {
     if (slow) op = (rd(sm, L, pc) << 8) | rd(sm, L, pc + 1);
   }
-  // ---- decode
-  const uint32_t hi = op >> 12, cm = 1u << hi, x = (op >> 8) & 15u, y = (op >> 4) & 15u, n = op & 15u,
-                 nn = op & 255u, nnn = op & 0xFFFu;
+  // ---- decode: one descriptor load replaces the per-class opcode compares
+  const uint32_t x = (op >> 8) & 15u, y = (op >> 4) & 15u, n = op & 15u, nn = op & 255u,
+                 nnn = op & 0xFFFu;
+  const uint32_t d = sm.dtab[desc_index(op)];
   const uint32_t vx = VREG(x), vy = VREG(y);
-  const bool isF = hi == 0xFu;
-  const bool f07 = isF & (nn == 0x07u), f0a = isF & (nn == 0x0Au), f15 = isF & (nn == 0x15u),
-             f18 = isF & (nn == 0x18u), f1e = isF & (nn == 0x1Eu), f29 = isF & (nn == 0x29u),
-             f33 = isF & (nn == 0x33u), f55 = isF & (nn == 0x55u), f65 = isF & (nn == 0x65u);
-  const bool is_ret = op == 0x00EEu, is_cls = op == 0x00E0u, is_call = hi == 2u;
-  const bool c59 = (cm & 0x0220u) != 0u;  // 5XY0 / 9XY0
+  const bool is_ret = op == 0x00EEu, is_cls = op == 0x00E0u;
   // ---- faults halt the lane (A17, A20)
-  bool bad = oob;
-  bad |= c59 & (n != 0u);
-  bad |= (hi == 8u) & (n > 7u) & (n != 0xEu);
-  bad |= (hi == 0xEu) & (nn != 0x9Eu) & (nn != 0xA1u);
-  bad |= isF & !(f07 | f0a | f15 | f18 | f1e | f29 | f33 | f55 | f65);
+  bool bad = oob | ((d & D_OK) == 0u) | (((d & D_NNCHK) != 0u) & (nn != (d >> 24)));
   bad |= is_ret & (L.sp == 0u);
-  bad |= is_call & (L.sp == 16u);
+  bad |= ((d & D_CALL) != 0u) & (L.sp == 16u);
   L.halted |= (uint32_t)(act & bad);
   act = act & !bad;
   // ---- stack
   uint32_t ret_pc = 0;
   if (act & is_ret) ret_pc = sm.stk[(L.sp - 1u) * kBlock + tid];
-  if (act & is_call) { sm.stk[L.sp * kBlock + tid] = (uint16_t)(pc + 2u); L.stk_dirty = 1; }
+  if (act & ((d & D_CALL) != 0u)) { sm.stk[L.sp * kBlock + tid] = (uint16_t)(pc + 2u); L.stk_dirty = 1; }
   // ---- skips: 3XNN 5XY0 on equal, 4XNN 9XY0 on not-equal, EX9E / EXA1 on key
-  const bool eq = vx == (c59 ? vy : nn);
+  const bool eq = vx == ((d & D_BVY) ? vy : nn);
   const bool keyd = ((L.keys >> (vx & 15u)) & 1u) != 0u;
-  const bool skip = (((cm & 0x0028u) != 0u) & eq) | (((cm & 0x0210u) != 0u) & !eq) |
-                    ((hi == 0xEu) & (keyd ^ (nn == 0xA1u)));
-  // ---- ALU 8XYn; flag written after the result (A15)
+  const bool skip = (((d & D_SKIPEQ) != 0u) & eq) | (((d & D_SKIPNE) != 0u) & !eq) |
+                    (((d & D_SKIPKEY) != 0u) & keyd) | (((d & D_SKIPNKEY) != 0u) & !keyd);
+  // ---- ALU 8XYn; flag written after the result (A15); VF-reset quirk folded into D_WVF
   const uint32_t s = (quirks & 1u) ? vy : vx;
   const bool sub5 = n == 5u, sub7 = n == 7u;
   const uint32_t sa = sub7 ? vy : vx;
@@ -307,34 +300,33 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   f8 = (n == 6u) ? (s & 1u) : f8;
   r8 = (n == 0xEu) ? ((s << 1) & 255u) : r8;
   f8 = (n == 0xEu) ? (s >> 7) : f8;
-  const bool is8 = hi == 8u;
-  const bool wvf = act & is8 & ((n >= 4u) | (((quirks & 16u) != 0u) & (n >= 1u)));
   // ---- register writes
   uint32_t nvx = nn;
-  nvx = (hi == 7u) ? ((vx + nn) & 255u) : nvx;
-  nvx = is8 ? r8 : nvx;
-  nvx = f07 ? L.dt : nvx;
-  nvx = f0a ? (uint32_t)(__ffs(L.keys) - 1) : nvx;
-  const bool wvx = act & (((cm & 0x01C0u) != 0u) | f07 | (f0a & (L.keys != 0u)));
+  nvx = (d & D_VSADD) ? ((vx + nn) & 255u) : nvx;
+  nvx = (d & D_VSALU) ? r8 : nvx;
+  nvx = (d & D_VSDT) ? L.dt : nvx;
+  nvx = (d & D_WAIT) ? (uint32_t)(__ffs(L.keys) - 1) : nvx;
+  const bool wvx = act & (((d & D_WVX) != 0u) | (((d & D_WAIT) != 0u) & (L.keys != 0u)));
   if (wvx) VREG(x) = (uint8_t)nvx;
-  if (wvf) VREG(15) = (uint8_t)f8;
+  if (act & ((d & D_WVF) != 0u)) VREG(15) = (uint8_t)f8;
   // ---- control flow and index / timer registers
   uint32_t npc = pc + (skip ? 4u : 2u);
-  npc = ((cm & 0x0006u) != 0u) ? nnn : npc;  // 1NNN, 2NNN
+  npc = (d & D_PCJ) ? nnn : npc;  // 1NNN, 2NNN
   npc = is_ret ? ret_pc : npc;
-  npc = (f0a & (L.keys == 0u)) ? pc : npc;   // A16: FX0A re-executes while no key
-  if (act & (hi == 0xBu)) npc = (nnn + VREG((quirks & 4u) ? x : 0u)) & 0xFFFu;
+  npc = (((d & D_WAIT) != 0u) & (L.keys == 0u)) ? pc : npc;  // A16: FX0A re-executes while no key
+  if (act & ((d & D_BJMP) != 0u)) npc = (nnn + VREG((quirks & 4u) ? x : 0u)) & 0xFFFu;
   uint32_t I2 = L.I;
-  I2 = (hi == 0xAu) ? nnn : I2;
-  I2 = f1e ? ((I2 + vx) & 0xFFFFu) : I2;
-  I2 = f29 ? (0x50u + 5u * (vx & 15u)) : I2;
+  I2 = (d & D_INNN) ? nnn : I2;
+  I2 = (d & D_IADD) ? ((I2 + vx) & 0xFFFFu) : I2;
+  I2 = (d & D_IFONT) ? (0x50u + 5u * (vx & 15u)) : I2;
   if (act) {
     L.pc = npc & 0xFFFFu;
     L.I = I2;
-    L.sp = L.sp + (uint32_t)is_call - (uint32_t)is_ret;
-    L.dt = f15 ? vx : L.dt;
-    L.st = f18 ? vx : L.st;
+    L.sp = L.sp + (uint32_t)((d & D_CALL) != 0u) - (uint32_t)is_ret;
+    L.dt = (d & D_DTW) ? vx : L.dt;
+    L.st = (d & D_STW) ? vx : L.st;
   }
+  const bool f33 = nn == 0x33u, f55 = nn == 0x55u;  // only meaningful under D_MEM
   // ---- vote-gated rare classes
   const bool do_cls = act & is_cls;
   if (__any_sync(kFull, do_cls)) {
@@ -343,7 +335,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
       for (int r = 0; r < 32; ++r) sm.fb[tid * 32 + r] = 0;
     }
   }
-  const bool do_rnd = act & (hi == 0xCu);
+  const bool do_rnd = act & ((d & D_RND) != 0u);
   if (__any_sync(kFull, do_rnd)) {
     if (do_rnd) {
       const uint32_t r = philox_out0(L.draw, L.episode, gid, 0u, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
@@ -351,7 +343,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
       L.draw++;
     }
   }
-  const bool do_mem = act & (f33 | f55 | f65);
+  const bool do_mem = act & ((d & D_MEM) != 0u);
   if (__any_sync(kFull, do_mem)) {
     if (do_mem) {
       if (f33) {
@@ -369,7 +361,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     }
     wdirty = __any_sync(kFull, L.dirty != 0ull);
   }
-  const bool do_draw = act & (hi == 0xDu);
+  const bool do_draw = act & ((d & D_DRAW) != 0u);
   if (__any_sync(kFull, do_draw)) {
     const uint32_t y0 = vy & 31u;
     const uint32_t nrows = do_draw ? (((quirks & 8u) != 0u) ? n : min(n, 32u - y0)) : 0u;
