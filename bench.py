@@ -304,21 +304,27 @@ def main():
     if im_t and im_t.get("envs") == n and im_t.get("dram_bytes_per_launch"):
         traffic = im_t["dram_bytes_per_launch"]   # ncu --set full, same launch configuration
 
-    issue = None
+    # ALU-pipe roof (the binding one): 148 SMs x 4 SMSPs x one
+    # ALU-pipe warp instruction per 2 cycles (B300_MICROARCH: alu pipe rt_SMSP = 2) x 32
+    # lanes x the SM clock sampled during the timed region; the work per env step is the
+    # kernel's ALU-pipe instruction count measured by ncu (profiles/latest_step_full.json).
+    alu = None
     im = issue_model(args.game, n)
-    if im and im.get("warp_instr_per_env_step"):
-        clk_mhz = None
-        try:
-            clk_mhz = clk.summary()["sm_mhz"]
-        except Exception:
-            pass
-        f_sm = (clk_mhz or 1965.0) * 1e6
-        peak_wi = 148 * 4 * f_sm  # warp instructions / s: 148 SMs x 4 schedulers x 1 issue/clk
-        wi = im["warp_instr_per_env_step"]
-        issue = {"warp_instr_per_env_step": wi, "source": im.get("source"),
-                 "peak_warp_instr_per_s": peak_wi, "roof_env_steps_per_s": peak_wi / wi,
-                 "frac": value / world / (peak_wi / wi),
-                 "warp_exec_efficiency": im.get("warp_exec_efficiency")}
+    clk_mhz = None
+    try:
+        clk_mhz = clk.summary()["sm_mhz"]
+    except Exception:
+        pass
+    f_sm = (clk_mhz or 1965.0) * 1e6
+    if im and im.get("alu_warp_instr_per_env_step"):
+        peak_alu = 148 * 4 * 0.5 * 32 * f_sm / 1e9          # G thread-ALU-ops / s
+        ach_alu = im["alu_warp_instr_per_env_step"] * 32 * value / world / 1e9
+        alu = {"achieved": ach_alu, "peak": peak_alu, "unit": "G ALU-pipe thread-instr/s",
+               "frac": ach_alu / peak_alu, "alu_warp_instr_per_env_step": im["alu_warp_instr_per_env_step"],
+               "all_warp_instr_per_env_step": im.get("warp_instr_per_env_step"),
+               "warp_exec_efficiency": im.get("warp_exec_efficiency"),
+               "ncu_alu_pipe_pct_of_peak": im.get("alu_pipe_pct_of_peak"),
+               "sm_mhz": f_sm / 1e6, "source": im.get("source")}
 
     # ---- e2e through the host-buffer C-ABI call (H2D actions, D2H obs/reward/done)
     e2e = None
@@ -365,6 +371,21 @@ def main():
         sweep.append({"envs_per_gpu": n, "steps_per_s_launch": value, "frames_per_s_launch": 4 * value,
                       "ms_per_step_launch": t_max / args.steps})
 
+    # ---- per-game throughput at BASELINE configs[3]'s size (262,144 envs per GPU): the
+    #      paper claims one number for all games; a SIMT interpreter is game dependent
+    games = []
+    if not args.no_sweep:
+        m = min(n, 262144)
+        for g in ("pong_standin", "brix_standin", "target_shooter_level1", "target_shooter_level2",
+                  "target_shooter_level3"):
+            grom, gspec = workloads.game(g)
+            tm, _, _ = time_config(grom, gspec, m, args.steps, args.warmup, odist.shard(rank, world, m)[0],
+                                   workloads.ACTION_SEED, torch, OctaxEnv, barrier)
+            tt = float(odist.max_over_ranks(torch.tensor([tm], dtype=torch.float64, device="cuda")).item())
+            sps = world * m * args.steps / (tt / 1e3)
+            games.append({"game": g, "envs_per_gpu": m, "steps_per_s": sps, "frames_per_s": 4 * sps,
+                          "source": "paper listing (App. D)" if g.startswith("target") else "labelled stand-in"})
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         vals, C, sample = oracle_throughput(args.game, 256, 400)
@@ -386,18 +407,24 @@ def main():
                        "obs_format": "packed [n,4,32,8]", "parallelism": f"env-sharded x{world}",
                        "l2": f"inputs larger than L2: ~{ALG_BYTES_PER_ENV_STEP * n / 2**30:.2f} GiB "
                              "touched per step vs 126 MB L2 (no flush needed)"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": traffic,
-                         "kernel": "octax_kernel<MODE_STEP>", "kernel_ms_median": kernel_ms,
-                         "alg_bytes_per_env_step": ALG_BYTES_PER_ENV_STEP, "peak_source": peak_src,
-                         "hbm_roof_env_steps_per_s": hbm_peak * 1e9 / ALG_BYTES_PER_ENV_STEP,
-                         "issue": issue},
+            "roofline": ({"bound": "alu", "achieved": alu["achieved"], "peak": alu["peak"], "unit": alu["unit"],
+                          "frac": alu["frac"], "traffic": traffic, "kernel": "octax_kernel<MODE_STEP>",
+                          "kernel_ms_median": kernel_ms, "alu": alu,
+                          "hbm": {"achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                                  "alg_bytes_per_env_step": ALG_BYTES_PER_ENV_STEP, "peak_source": peak_src,
+                                  "roof_env_steps_per_s": hbm_peak * 1e9 / ALG_BYTES_PER_ENV_STEP}}
+                         if alu else
+                         {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                          "frac": achieved / hbm_peak, "traffic": traffic, "kernel": "octax_kernel<MODE_STEP>",
+                          "kernel_ms_median": kernel_ms, "alg_bytes_per_env_step": ALG_BYTES_PER_ENV_STEP,
+                          "peak_source": peak_src}),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "stats": [int(x) for x in st.cpu().tolist()],
             "sweep": sweep,
+            "games": games,
             "paper_context": PAPER_CONTEXT,
         }
         print(json.dumps(out), flush=True)

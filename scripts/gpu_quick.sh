@@ -11,7 +11,7 @@ python - <<'PY'
 import json
 try:
     d = json.load(open("gpurun_out/bench.json"))
-    print("value %.4g steps/s  ms/step %.3f  frac %.3f  clocks %s" % (d["value"], d["ms_per_step"], d["roofline"]["frac"], d["clocks"]))
+    print("value %.4g steps/s  ms/step %.3f  bound %s frac %.3f  clocks %s" % (d["value"], d["ms_per_step"], d["roofline"]["bound"], d["roofline"]["frac"], d["clocks"]))
     for s in d.get("sweep", []): print("  sweep", s)
 except Exception as e:
     print("bench parse failed", e); print(open("gpurun_out/bench.err").read()[-2000:])

@@ -20,6 +20,10 @@ KEY_METRICS = [
     "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.sum",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__cycles_active.sum",
+    "sm__inst_executed_pipe_fma.sum",
     "smsp__inst_executed.sum",
     "smsp__thread_inst_executed.sum",
     "dram__bytes_read.sum",
@@ -88,6 +92,13 @@ def full(path, out, extra):
             r0 = res[0]
             js["warp_instr_per_env_step"] = float(r0["smsp__inst_executed.sum"]["value"]) / extra["envs"]
             js["warp_exec_efficiency"] = float(r0["smsp__thread_inst_executed_per_inst_executed.ratio"]["value"]) / 32
+            pct = float(r0["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"]["value"])
+            js["alu_pipe_pct_of_peak"] = pct
+            if "sm__inst_executed_pipe_alu.sum" in r0:
+                alu = float(r0["sm__inst_executed_pipe_alu.sum"]["value"])
+            else:  # ALU pipe peak = 2 warp instr / SM / cycle (4 SMSPs x 1 per 2 cycles)
+                alu = pct / 100.0 * 2.0 * float(r0["sm__cycles_active.sum"]["value"])
+            js["alu_warp_instr_per_env_step"] = alu / extra["envs"]
             if "dram_bytes_per_launch" in js:
                 js["dram_bytes_per_env_step"] = js["dram_bytes_per_launch"] / extra["envs"]
         except Exception:

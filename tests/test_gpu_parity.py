@@ -83,7 +83,9 @@ def test_coverage_rom_n1_1000_steps_full_state_every_step():
 
 
 # ---------------------------------------------------------------- stand-in games, ragged n
-@pytest.mark.parametrize("game,n", [("pong_standin", 300), ("brix_standin", 257), ("brix_standin", 1)])
+@pytest.mark.parametrize("game,n", [("pong_standin", 300), ("brix_standin", 257), ("brix_standin", 1),
+                                    ("target_shooter_level1", 200), ("target_shooter_level2", 333),
+                                    ("target_shooter_level3", 129)])
 def test_game_parity(game, n):
     rom, spec = workloads.game(game)
     _run_parity(rom, spec, n, 300, 77, 5)

@@ -68,6 +68,11 @@ def game(name: str, **over) -> tuple[bytes, dict]:
         p = PAPER_SPECS["pong"]
         spec = dict(DEFAULTS, score=p["score"], terminated=p["terminated"],
                     action_keys=p["action_keys"])
+    elif name.startswith("target_shooter_level"):
+        # the paper's own game (App. D), spec from its wrapper listing:
+        # score V[2], terminated V[3] == 1, action_set [5,7,8,9,6]
+        p = PAPER_SPECS["target_shooter"]
+        spec = dict(DEFAULTS, score=p["score"], terminated=p["terminated"], action_keys=p["action_keys"])
     elif name == "brix_standin":
         p = PAPER_SPECS["brix"]
         spec = dict(DEFAULTS, score=p["score"], terminated=p["terminated"],
