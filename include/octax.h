@@ -139,6 +139,25 @@ octax_status octax_reset(octax_env *e, uint64_t seed, void *obs_out);
 octax_status octax_step(octax_env *e, const int32_t *actions, void *obs_out, float *reward_out,
                         uint8_t *done_out, uint8_t *terminated_out, uint8_t *truncated_out);
 
+/* Optional extra outputs of octax_step_ex (all DEVICE buffers, each may be NULL):
+ *  final_obs_out       obs of the TERMINAL transition (the 4 stacked displays before the
+ *                      same-step auto-reset, A10), same layout as obs_out; written for envs
+ *                      with done = 1 only, other rows untouched.  With it a caller gets
+ *                      SPEC's final-observation convention on top of Gymnax's.
+ *  episode_return_out  int32 [n]: return (sum of rewards) of the episode that ended this
+ *                      step, 0 where done = 0 (S:417 telescoping).
+ *  episode_length_out  uint32 [n]: its length in steps, 0 where done = 0. */
+typedef struct {
+  void *final_obs_out;
+  int32_t *episode_return_out;
+  uint32_t *episode_length_out;
+} octax_step_extras;
+
+/* octax_step plus the extras above (extras may be NULL = octax_step). */
+octax_status octax_step_ex(octax_env *e, const int32_t *actions, void *obs_out, float *reward_out,
+                           uint8_t *done_out, uint8_t *terminated_out, uint8_t *truncated_out,
+                           const octax_step_extras *extras);
+
 /* Same step with HOST buffers (pinned recommended): copies actions host->device,
  * runs octax_step on internal device buffers, copies obs/reward/done back and
  * synchronises.  terminated_out / truncated_out may be NULL. */

@@ -70,6 +70,7 @@ def lib():
                                           ctypes.POINTER(P)]
         L.octax_oracle_reset.argtypes = [P, ctypes.c_uint64, P]
         L.octax_oracle_step.argtypes = [P, P, P, P, P, P, P]
+        L.octax_oracle_step_ex.argtypes = [P, P, P, P, P, P, P, P, P, P]
         L.octax_oracle_stats.argtypes = [P, P]
         L.octax_oracle_get_state.argtypes = [P, ctypes.c_uint64, P]
         L.octax_oracle_set_state.argtypes = [P, ctypes.c_uint64, P]
@@ -167,6 +168,19 @@ class OracleEnv:
         _check(lib().octax_oracle_step(self._h, _ptr(a), _ptr(obs), _ptr(rew), _ptr(done),
                                        _ptr(term), _ptr(trunc)))
         return obs, rew, done, term, trunc
+
+    def step_ex(self, actions):
+        """Step plus extras: (obs, reward, done, term, trunc, final_obs, ep_return, ep_length)."""
+        a = np.ascontiguousarray(actions, dtype=np.int32)
+        obs = np.zeros((self.n, self.obs_per_env), np.uint8)
+        fin = np.zeros((self.n, self.obs_per_env), np.uint8)
+        rew = np.zeros(self.n, np.float32)
+        done, term, trunc = (np.zeros(self.n, np.uint8) for _ in range(3))
+        er = np.zeros(self.n, np.int32)
+        el = np.zeros(self.n, np.uint32)
+        _check(lib().octax_oracle_step_ex(self._h, _ptr(a), _ptr(obs), _ptr(rew), _ptr(done), _ptr(term),
+                                          _ptr(trunc), _ptr(fin), _ptr(er), _ptr(el)))
+        return obs, rew, done, term, trunc, fin, er, el
 
     def step_into(self, actions, obs, rew, done, term=None, trunc=None) -> None:
         """Step writing into caller-provided (preallocated) numpy buffers."""

@@ -781,10 +781,14 @@ int octax_oracle_reset(oracle_env *e, uint64_t seed, uint8_t *obs_out) {
   return ORACLE_OK;
 }
 
-/* step(j, a): SURVEY c.1 "step" -- P:146, A5-A10, A25 */
-int octax_oracle_step(oracle_env *e, const int32_t *actions, uint8_t *obs_out,
-                      float *reward_out, uint8_t *done_out,
-                      uint8_t *terminated_out, uint8_t *truncated_out) {
+/* step(j, a): SURVEY c.1 "step" -- P:146, A5-A10, A25.
+   Optional extras: final_obs_out (the obs of the terminal transition, written for
+   done envs only), episode_return_out / episode_length_out (0 where not done). */
+int octax_oracle_step_ex(oracle_env *e, const int32_t *actions, uint8_t *obs_out,
+                         float *reward_out, uint8_t *done_out,
+                         uint8_t *terminated_out, uint8_t *truncated_out,
+                         uint8_t *final_obs_out, int32_t *episode_return_out,
+                         uint32_t *episode_length_out) {
   if (!e || !actions) return fail(ORACLE_E_INVALID_ARG, "NULL argument");
   for (uint64_t j = 0; j < e->n; j++) {
     vm *m = &e->vms[j];
@@ -810,7 +814,10 @@ int octax_oracle_step(oracle_env *e, const int32_t *actions, uint8_t *obs_out,
     memmove(m->hist[2], m->hist[3], sizeof m->hist[0]);
     memcpy(m->hist[3], m->disp, sizeof m->disp);
     e->stats[2] += 1;
+    if (episode_return_out) episode_return_out[j] = (term || trunc) ? m->ep_ret : 0;
+    if (episode_length_out) episode_length_out[j] = (term || trunc) ? m->steps : 0u;
     if (term || trunc) { /* A10: same-step auto-reset, Gymnax convention */
+      if (final_obs_out) write_obs(e, m, final_obs_out + j * obs_bytes(e));
       e->stats[0] += m->ep_ret;
       e->stats[1] += 1;
       m->episode++;
@@ -823,6 +830,13 @@ int octax_oracle_step(oracle_env *e, const int32_t *actions, uint8_t *obs_out,
     if (truncated_out) truncated_out[j] = trunc ? 1 : 0;
   }
   return ORACLE_OK;
+}
+
+int octax_oracle_step(oracle_env *e, const int32_t *actions, uint8_t *obs_out,
+                      float *reward_out, uint8_t *done_out,
+                      uint8_t *terminated_out, uint8_t *truncated_out) {
+  return octax_oracle_step_ex(e, actions, obs_out, reward_out, done_out, terminated_out,
+                              truncated_out, NULL, NULL, NULL);
 }
 
 int octax_oracle_stats(oracle_env *e, int64_t out4[4]) {

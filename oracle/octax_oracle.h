@@ -82,6 +82,11 @@ int octax_oracle_reset(oracle_env *e, uint64_t seed, uint8_t *obs_out);
 int octax_oracle_step(oracle_env *e, const int32_t *actions, uint8_t *obs_out,
                       float *reward_out, uint8_t *done_out,
                       uint8_t *terminated_out, uint8_t *truncated_out);
+int octax_oracle_step_ex(oracle_env *e, const int32_t *actions, uint8_t *obs_out,
+                         float *reward_out, uint8_t *done_out,
+                         uint8_t *terminated_out, uint8_t *truncated_out,
+                         uint8_t *final_obs_out, int32_t *episode_return_out,
+                         uint32_t *episode_length_out);
 int octax_oracle_stats(oracle_env *e, int64_t out4[4]);
 int octax_oracle_get_state(oracle_env *e, uint64_t env, uint8_t *canon_out);
 int octax_oracle_set_state(oracle_env *e, uint64_t env, const uint8_t *canon_in);

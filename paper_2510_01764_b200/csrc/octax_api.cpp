@@ -23,7 +23,8 @@ cudaError_t launch_step(const StepParams &p, int mode, const int32_t *actions, u
                         uint8_t *done, uint8_t *term, uint8_t *trunc, cudaStream_t stream);
 cudaError_t launch_gen_actions(uint64_t n, uint64_t env_offset, uint64_t aseed, uint64_t t, uint32_t n_actions,
                                int32_t *out, cudaStream_t stream);
-cudaError_t launch_expand_obs(uint64_t n, const uint8_t *packed, uint8_t *dense, cudaStream_t stream);
+cudaError_t launch_expand_obs(uint64_t n, const uint8_t *packed, uint8_t *dense, cudaStream_t stream,
+                              const uint8_t *row_mask = nullptr);
 cudaError_t launch_get_states(const StepParams &p, const uint64_t *ids, uint64_t count, uint8_t *out,
                               cudaStream_t stream);
 cudaError_t launch_set_state(const StepParams &p, uint64_t env, const uint8_t *canon, cudaStream_t stream);
@@ -356,6 +357,7 @@ struct octax_env {
   void *block = nullptr;          // one allocation holding all per-env state
   size_t block_bytes = 0;
   uint8_t *packed_scratch = nullptr;  // packed obs staging for the bool format
+  uint8_t *final_scratch = nullptr;   // packed final-obs staging for the bool format (lazy)
   // host-step staging (lazy)
   int32_t *d_actions = nullptr;
   uint8_t *d_obs = nullptr;
@@ -374,6 +376,7 @@ static void free_env(octax_env *e) {
   cudaSetDevice(e->device);
   cudaFree(e->block);
   cudaFree(e->packed_scratch);
+  cudaFree(e->final_scratch);
   cudaFree(e->d_actions);
   cudaFree(e->d_obs);
   cudaFree(e->d_reward);
@@ -502,18 +505,43 @@ extern "C" octax_status octax_reset(octax_env *e, uint64_t seed, void *obs_out) 
   return OCTAX_OK;
 }
 
-extern "C" octax_status octax_step(octax_env *e, const int32_t *actions, void *obs_out, float *reward_out,
-                                   uint8_t *done_out, uint8_t *terminated_out, uint8_t *truncated_out) {
+extern "C" octax_status octax_step_ex(octax_env *e, const int32_t *actions, void *obs_out, float *reward_out,
+                                      uint8_t *done_out, uint8_t *terminated_out, uint8_t *truncated_out,
+                                      const octax_step_extras *extras) {
   if (!e || !actions || !obs_out || !reward_out || !done_out)
     return set_err(OCTAX_E_INVALID_ARG, "NULL argument to octax_step");
   DeviceGuard g(e->device);
   uint8_t *packed = e->obs_format == OCTAX_OBS_PACKED ? (uint8_t *)obs_out : e->packed_scratch;
-  CU(launch_step(e->p, MODE_STEP, actions, packed, reward_out, done_out, terminated_out, truncated_out, e->stream),
+  StepParams p = e->p;
+  p.final_obs = nullptr;
+  p.ep_ret_out = nullptr;
+  p.ep_len_out = nullptr;
+  if (extras) {
+    p.ep_ret_out = extras->episode_return_out;
+    p.ep_len_out = extras->episode_length_out;
+    if (extras->final_obs_out) {
+      if (e->obs_format == OCTAX_OBS_PACKED) {
+        p.final_obs = (uint8_t *)extras->final_obs_out;
+      } else {
+        if (!e->final_scratch) CU(cudaMalloc(&e->final_scratch, 1024 * e->n), "cudaMalloc(final obs scratch)");
+        p.final_obs = e->final_scratch;
+      }
+    }
+  }
+  CU(launch_step(p, MODE_STEP, actions, packed, reward_out, done_out, terminated_out, truncated_out, e->stream),
      "step kernel");
-  if (e->obs_format != OCTAX_OBS_PACKED)
+  if (e->obs_format != OCTAX_OBS_PACKED) {
     CU(launch_expand_obs(e->n, packed, (uint8_t *)obs_out, e->stream), "expand obs");
+    if (p.final_obs)
+      CU(launch_expand_obs(e->n, p.final_obs, (uint8_t *)extras->final_obs_out, e->stream, done_out), "expand final obs");
+  }
   e->p.head = (e->p.head + 1) & 3u;
   return OCTAX_OK;
+}
+
+extern "C" octax_status octax_step(octax_env *e, const int32_t *actions, void *obs_out, float *reward_out,
+                                   uint8_t *done_out, uint8_t *terminated_out, uint8_t *truncated_out) {
+  return octax_step_ex(e, actions, obs_out, reward_out, done_out, terminated_out, truncated_out, nullptr);
 }
 
 extern "C" octax_status octax_step_host(octax_env *e, const int32_t *actions_host, void *obs_host,

@@ -71,6 +71,10 @@ struct DevState {
 
 struct StepParams {
   DevState s;
+  // optional per-step extra outputs (octax_step_ex), nullptr when not requested
+  uint8_t *final_obs;      // packed [n][4][32][8]: obs of the terminal transition, done envs only
+  int32_t *ep_ret_out;     // return of the episode that ended this step (0 if none)
+  uint32_t *ep_len_out;    // its length in steps (0 if none)
   uint64_t n;
   uint64_t env_offset;
   uint64_t seed;

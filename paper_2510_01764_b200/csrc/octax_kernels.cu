@@ -565,6 +565,25 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       if (trunc_out) trunc_out[env] = (uint8_t)trunc;
     }
     resetting = active && done;
+    // ---- optional extras: the terminal transition's obs and the finished episode's return/length
+    if (active && p.ep_ret_out) p.ep_ret_out[env] = done ? ep_ret : 0;
+    if (active && p.ep_len_out) p.ep_len_out[env] = done ? steps : 0u;
+    if (p.final_obs) {
+      __syncwarp();
+      uint32_t dm = __ballot_sync(kFull, resetting);
+      uint64_t *fo64 = reinterpret_cast<uint64_t *>(p.final_obs);
+      while (dm) {
+        const int e = __ffs(dm) - 1;
+        dm &= dm - 1;
+        const uint64_t *rg = ring + (wbase + e) * 128;
+        uint64_t *fo = fo64 + (wbase + e) * 128;
+        fo[lane] = rg[s0 * 32 + lane];
+        fo[32 + lane] = rg[s1 * 32 + lane];
+        fo[64 + lane] = rg[s2 * 32 + lane];
+        fo[96 + lane] = sm.fb[fb_idx(warp * 32 + e, lane)];
+      }
+      __syncwarp();
+    }
   } else {
     resetting = active;
     L.episode = 0;
@@ -665,10 +684,12 @@ __global__ void gen_actions_kernel(uint64_t n, uint64_t env_offset, uint64_t ase
 }
 
 // packed [n][4][32][8] -> bool [n][4][64][32]; one thread writes 16 bytes (16 y's of one x)
-__global__ void expand_obs_kernel(uint64_t n, const uint8_t *__restrict__ packed, uint8_t *__restrict__ dense) {
+__global__ void expand_obs_kernel(uint64_t n, const uint8_t *__restrict__ packed, uint8_t *__restrict__ dense,
+                                  const uint8_t *__restrict__ row_mask) {
   uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;  // unit of 16 output bytes
   uint64_t total = n * 4 * 64 * 2;
   if (i >= total) return;
+  if (row_mask && !row_mask[i >> 9]) return;  // 512 units of 16 B per env
   uint32_t yh = i & 1, x = (i >> 1) & 63;
   uint64_t plane = i >> 7;  // env*4 + p
   const uint8_t *src = packed + plane * 256;
@@ -783,10 +804,11 @@ cudaError_t launch_gen_actions(uint64_t n, uint64_t env_offset, uint64_t aseed, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_expand_obs(uint64_t n, const uint8_t *packed, uint8_t *dense, cudaStream_t stream) {
+cudaError_t launch_expand_obs(uint64_t n, const uint8_t *packed, uint8_t *dense, cudaStream_t stream,
+                              const uint8_t *row_mask) {
   uint64_t total = n * 4 * 64 * 2;
   const unsigned grid = (unsigned)((total + 255) / 256);
-  expand_obs_kernel<<<grid, 256, 0, stream>>>(n, packed, dense);
+  expand_obs_kernel<<<grid, 256, 0, stream>>>(n, packed, dense, row_mask);
   return cudaGetLastError();
 }
 

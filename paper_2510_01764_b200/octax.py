@@ -20,7 +20,7 @@ OBS_BOOL_XMAJOR = 1
 
 # every symbol include/octax.h declares
 SYMBOLS = (
-    "octax_create", "octax_reset", "octax_step", "octax_step_host", "octax_gen_actions",
+    "octax_create", "octax_reset", "octax_step", "octax_step_ex", "octax_step_host", "octax_gen_actions",
     "octax_stats", "octax_stats_device", "octax_get_state", "octax_get_states",
     "octax_set_state", "octax_info", "octax_destroy", "octax_last_error",
 )
@@ -53,6 +53,11 @@ class _Spec(ctypes.Structure):
     ]
 
 
+class _Extras(ctypes.Structure):
+    _fields_ = [("final_obs_out", ctypes.c_void_p), ("episode_return_out", ctypes.c_void_p),
+                ("episode_length_out", ctypes.c_void_p)]
+
+
 class _Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("cuda_stream", ctypes.c_void_p),
                 ("env_offset", ctypes.c_uint64), ("total_envs", ctypes.c_uint64)]
@@ -74,6 +79,7 @@ def load_library():
                                ctypes.POINTER(_Opts), ctypes.POINTER(P)]
     L.octax_reset.argtypes = [P, u64, P]
     L.octax_step.argtypes = [P, P, P, P, P, P, P]
+    L.octax_step_ex.argtypes = [P, P, P, P, P, P, P, ctypes.POINTER(_Extras)]
     L.octax_step_host.argtypes = [P, P, P, P, P, P, P]
     L.octax_gen_actions.argtypes = [P, u64, u64, P]
     L.octax_stats.argtypes = [P, P]
@@ -187,6 +193,20 @@ class OctaxEnv:
 
     def step(self, actions):
         self.step_into(actions, self.obs, self.reward, self.done, self.terminated, self.truncated)
+        return self.obs, self.reward, self.done
+
+    def step_ex(self, actions, final_obs=None, episode_return=None, episode_length=None):
+        """Step with the optional extras of octax_step_ex (terminal obs of done envs,
+        return / length of the episodes that ended this step)."""
+        import torch
+        ex = _Extras(None if final_obs is None else _dptr(final_obs, torch.uint8, self.n * self.obs_per_env).value,
+                     None if episode_return is None else _dptr(episode_return, torch.int32, self.n).value,
+                     None if episode_length is None else _dptr(episode_length, torch.int32, self.n).value)
+        _check(load_library().octax_step_ex(
+            self._h, _dptr(actions, torch.int32, self.n), _dptr(self.obs, torch.uint8, self.n * self.obs_per_env),
+            _dptr(self.reward, torch.float32, self.n), _dptr(self.done, torch.uint8, self.n),
+            _dptr(self.terminated, torch.uint8, self.n), _dptr(self.truncated, torch.uint8, self.n),
+            ctypes.byref(ex)))
         return self.obs, self.reward, self.done
 
     def step_host(self, actions: np.ndarray, obs: np.ndarray, reward: np.ndarray, done: np.ndarray,

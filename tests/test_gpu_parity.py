@@ -318,3 +318,57 @@ def test_cuda_graph_capture_matches_eager():
     ids = list(range(0, n, 7))
     assert np.array_equal(graphed.get_states(ids), ref.get_states(ids))
     assert np.array_equal(graphed.obs.cpu().numpy(), ref.obs.cpu().numpy())
+
+
+@pytest.mark.parametrize("obs_format", [0, 1])
+def test_step_ex_final_obs_and_episode_info(obs_format):
+    """octax_step_ex extras vs the oracle: terminal obs of done envs (SPEC S:409
+    convention), return and length of the finished episodes."""
+    rom, spec = workloads.game("brix_standin", obs_format=obs_format, max_episode_steps=45)
+    n = 300
+    g = _gpu_env(rom, spec, n, 21)
+    o = oracle.OracleEnv(rom, spec, n, 21)
+    per = g.obs_per_env
+    fin = torch.zeros(n * per, dtype=torch.uint8, device="cuda")
+    er = torch.zeros(n, dtype=torch.int32, device="cuda")
+    el = torch.zeros(n, dtype=torch.int32, device="cuda")
+    seen = 0
+    for t in range(120):
+        acts = workloads.gen.actions(21, t, n, 3)
+        g.step_ex(torch.from_numpy(acts).cuda(), final_obs=fin, episode_return=er, episode_length=el)
+        oo, orw, od, ot, otr, ofin, oer, oel = o.step_ex(acts)
+        assert np.array_equal(g.obs.cpu().numpy().reshape(n, -1), oo)
+        assert np.array_equal(g.done.cpu().numpy(), od)
+        assert np.array_equal(er.cpu().numpy(), oer)
+        assert np.array_equal(el.cpu().numpy().astype(np.uint32), oel)
+        d = od.astype(bool)
+        if d.any():
+            gf = fin.cpu().numpy().reshape(n, -1)
+            assert np.array_equal(gf[d], ofin[d])
+            seen += int(d.sum())
+    assert seen > 20
+
+
+def test_vec_env_wrapper_shapes_and_values():
+    from paper_2510_01764_b200.vec_env import OctaxVecEnv
+    rom, spec = workloads.game("brix_standin", max_episode_steps=30)
+    n = 64
+    env = OctaxVecEnv(rom, spec, n, seed=3, dense=True)
+    o = oracle.OracleEnv(rom, dict(spec, obs_format=1), n, 3)
+    obs, info = env.reset(seed=3)
+    assert obs.shape == (n, 4, 64, 32) and obs.dtype == torch.bool
+    assert np.array_equal(obs.cpu().numpy().reshape(n, -1).astype(np.uint8), o.reset(3))
+    for t in range(40):
+        acts = workloads.gen.actions(8, t, n, env.single_action_space.n)
+        obs, rew, term, trunc, info = env.step(torch.from_numpy(acts))
+        oo, orw, od, ot, otr, ofin, oer, oel = o.step_ex(acts)
+        assert np.array_equal(obs.cpu().numpy().reshape(n, -1).astype(np.uint8), oo)
+        assert np.array_equal(rew.cpu().numpy(), orw)
+        assert np.array_equal(term.cpu().numpy(), ot.astype(bool))
+        assert np.array_equal(trunc.cpu().numpy(), otr.astype(bool))
+        m = info["_final_obs"].cpu().numpy()
+        assert np.array_equal(m, od.astype(bool))
+        if m.any():
+            fo = info["final_obs"].cpu().numpy().reshape(n, -1).astype(np.uint8)
+            assert np.array_equal(fo[m], ofin[m])
+            assert np.array_equal(info["episode"]["r"].cpu().numpy()[m], oer[m])
