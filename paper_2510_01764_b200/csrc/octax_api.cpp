@@ -304,6 +304,7 @@ octax_status compile_expr(const char *src, const char *what, Program &prog) {
 // folded in.
 void build_desc_table(uint32_t quirks, uint32_t out[kDescEntries]) {
   for (uint32_t k = 0; k < kDescEntries; ++k) out[k] = 0;
+  const uint32_t shift_reads = (quirks & OCTAX_Q_SHIFT_VY) ? D_RY : D_RX;
   for (uint32_t hi = 0; hi < 14; ++hi)
     for (uint32_t n = 0; n < 16; ++n) {
       uint32_t d = 0;
@@ -311,30 +312,31 @@ void build_desc_table(uint32_t quirks, uint32_t out[kDescEntries]) {
         case 0x0: d = D_OK; break;  // 00E0 / 00EE / 0NNN decided from the full word
         case 0x1: d = D_OK | D_PCJ; break;
         case 0x2: d = D_OK | D_PCJ | D_CALL; break;
-        case 0x3: d = D_OK | D_SKIPEQ; break;
-        case 0x4: d = D_OK | D_SKIPNE; break;
-        case 0x5: d = n == 0 ? (D_OK | D_SKIPEQ | D_BVY) : 0u; break;
+        case 0x3: d = D_OK | D_SKIPEQ | D_RX; break;
+        case 0x4: d = D_OK | D_SKIPNE | D_RX; break;
+        case 0x5: d = n == 0 ? (D_OK | D_SKIPEQ | D_BVY | D_RX | D_RY) : 0u; break;
         case 0x6: d = D_OK | D_WVX; break;
-        case 0x7: d = D_OK | D_WVX | D_VSADD; break;
+        case 0x7: d = D_OK | D_WVX | D_VSADD | D_RX; break;
         case 0x8:
           if (n <= 7 || n == 0xE) {
             d = D_OK | D_WVX | D_VSALU;
             if (n >= 4 || ((quirks & OCTAX_Q_VF_RESET) && n >= 1)) d |= D_WVF;
+            d |= n == 0 ? D_RY : (n == 6 || n == 0xE) ? shift_reads : (D_RX | D_RY);
           }
           break;
-        case 0x9: d = n == 0 ? (D_OK | D_SKIPNE | D_BVY) : 0u; break;
+        case 0x9: d = n == 0 ? (D_OK | D_SKIPNE | D_BVY | D_RX | D_RY) : 0u; break;
         case 0xA: d = D_OK | D_INNN; break;
-        case 0xB: d = D_OK | D_BJMP; break;
+        case 0xB: d = D_OK | D_BJMP | ((quirks & OCTAX_Q_JUMP_VX) ? D_RX : 0u); break;
         case 0xC: d = D_OK | D_RND; break;
-        case 0xD: d = D_OK | D_DRAW; break;
+        case 0xD: d = D_OK | D_DRAW | D_RX | D_RY; break;
       }
       out[(hi << 4) | n] = d;
     }
   struct { uint32_t op; uint32_t d; } ef[] = {
-      {0xE09E, D_SKIPKEY}, {0xE0A1, D_SKIPNKEY}, {0xF007, D_WVX | D_VSDT}, {0xF00A, D_WAIT},
-      {0xF015, D_DTW},     {0xF018, D_STW},      {0xF01E, D_IADD},        {0xF029, D_IFONT},
-      {0xF033, D_MEM},     {0xF055, D_MEM},      {0xF065, D_MEM}};
-  for (auto &e : ef) out[desc_index(e.op)] = D_OK | D_NNCHK | e.d | ((e.op & 0xFFu) << 24);
+      {0xE09E, D_SKIPKEY | D_RX}, {0xE0A1, D_SKIPNKEY | D_RX}, {0xF007, D_WVX | D_VSDT}, {0xF00A, D_WAIT},
+      {0xF015, D_DTW | D_RX},     {0xF018, D_STW | D_RX},      {0xF01E, D_IADD | D_RX},  {0xF029, D_IFONT | D_RX},
+      {0xF033, D_MEM | D_RX},     {0xF055, D_MEM | D_RX},      {0xF065, D_MEM}};
+  for (auto &e : ef) out[desc_index(e.op)] = D_OK | D_YCHK | e.d | (((e.op >> 4) & 15u) << 28);
 }
 
 // Canonical CHIP-8 font, 16 glyphs x 5 rows, stored at 0x050 (A23).

@@ -17,13 +17,17 @@ constexpr uint32_t kStageBytes = kImageBytes + 4 * kDescEntries;  // image + dec
 // Per-handle decode table (quirks folded in), indexed by desc_index(op): one
 // 32-bit descriptor of what the instruction does, so the warp-uniform core tests
 // descriptor bits instead of re-deriving the class from the opcode every cycle.
-// E/F entries carry the full expected low byte (bits 24..31, checked under D_NNCHK).
+// E/F entries carry the expected y nibble (bits 28..31, checked under D_YCHK): with
+// the injective nibble hash below, (hi, hash, y) determines the whole word.
+// D_RX / D_RY: the instruction reads V[x] / V[y] (deferred-DXYN resolution trigger
+// when that register is VF and a queued draw's VF result is still pending).
 enum : uint32_t {
-  D_OK = 1u << 0, D_NNCHK = 1u << 1, D_SKIPEQ = 1u << 2, D_SKIPNE = 1u << 3, D_BVY = 1u << 4,
+  D_OK = 1u << 0, D_YCHK = 1u << 1, D_SKIPEQ = 1u << 2, D_SKIPNE = 1u << 3, D_BVY = 1u << 4,
   D_SKIPKEY = 1u << 5, D_SKIPNKEY = 1u << 6, D_WVX = 1u << 7, D_WVF = 1u << 8, D_VSADD = 1u << 9,
   D_VSALU = 1u << 10, D_VSDT = 1u << 11, D_WAIT = 1u << 12, D_PCJ = 1u << 13, D_CALL = 1u << 14,
   D_BJMP = 1u << 15, D_INNN = 1u << 16, D_IADD = 1u << 17, D_IFONT = 1u << 18, D_DTW = 1u << 19,
-  D_STW = 1u << 20, D_RND = 1u << 21, D_MEM = 1u << 22, D_DRAW = 1u << 23
+  D_STW = 1u << 20, D_RND = 1u << 21, D_MEM = 1u << 22, D_DRAW = 1u << 23,
+  D_RX = 1u << 24, D_RY = 1u << 25
 };
 
 // hi << 4 | low nibble; for EXnn / FXnn the nibble is (n - 2y) & 15, which is

@@ -142,8 +142,8 @@ __device__ __forceinline__ void power_on(Smem &sm, Lane &L, int tid) {
 // start bit at or below it (one REDUX.OR + FLO), so a pass costs no shuffle chain.
 __device__ __forceinline__ void draw_coop(Smem &sm, const Lane &L, const StepParams &p, int tid, int lane,
                                           uint64_t block0, bool do_draw, uint32_t x0, uint32_t y0, uint32_t base,
-                                          uint32_t n) {
-  const bool wrap = (p.quirks & 8u) != 0;
+                                          uint32_t n, bool vfw, uint32_t quirks) {
+  const bool wrap = (quirks & 8u) != 0;
   const uint32_t nrows = do_draw ? (wrap ? n : min(n, 32u - y0)) : 0u;
   const uint32_t lt = (1u << lane) - 1u;
   uint32_t excl = 0, total = 0;
@@ -193,7 +193,7 @@ __device__ __forceinline__ void draw_coop(Smem &sm, const Lane &L, const StepPar
     hitmask |= __reduce_or_sync(kFull, hit ? (1u << j) : 0u);
     __syncwarp();
   }
-  if (do_draw) VREG(15) = (uint8_t)((hitmask >> lane) & 1u);
+  if (vfw) VREG(15) = (uint8_t)((hitmask >> lane) & 1u);
 }
 
 // DXYN, lane-parallel: every drawing lane XORs its own rows, loop bound = the
@@ -204,7 +204,7 @@ __device__ __forceinline__ void draw_coop(Smem &sm, const Lane &L, const StepPar
 // leftmost), so the mask is built as bswap16(sprite << 8 >> (x0 & 7)) << 8*(x0 >> 3).
 __device__ __forceinline__ void draw_lanes(Smem &sm, Lane &L, const StepParams &p, int tid, bool do_draw,
                                            uint32_t x0, uint32_t y0, uint32_t base, uint32_t nrows, uint32_t maxr,
-                                           bool wdirty, uint32_t quirks) {
+                                           bool wdirty, uint32_t quirks, bool vfw) {
   const bool wrap = (quirks & 8u) != 0;
   bool slowb = do_draw & (base + 15u > 0xFFFu);
   if (wdirty) slowb |= do_draw & (((L.dirty >> (base >> 6)) & 3ull) != 0ull);
@@ -240,11 +240,9 @@ __device__ __forceinline__ void draw_lanes(Smem &sm, Lane &L, const StepParams &
       hit |= old & m;
     }
   }
-  if (do_draw) VREG(15) = (uint8_t)(hit != 0ull);
+  if (vfw) VREG(15) = (uint8_t)(hit != 0ull);
 }
 
-// One CHIP-8 cycle for every lane with `part` (must be called by all 32 lanes).
-// Branch-free predicated core; class tests are one-hot masks cm = 1 << (op >> 12).
 template <bool Q0>
 __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, int tid, int lane, uint64_t block0,
                                       uint32_t gid, bool part, bool &wdirty) {
@@ -264,14 +262,17 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   const uint32_t x = (op >> 8) & 15u, y = (op >> 4) & 15u, n = op & 15u, nn = op & 255u,
                  nnn = op & 0xFFFu;
   const uint32_t d = sm.dtab[desc_index(op)];
-  const uint32_t vx = VREG(x), vy = VREG(y);
   const bool is_ret = op == 0x00EEu, is_cls = op == 0x00E0u;
   // ---- faults halt the lane (A17, A20)
-  bool bad = oob | ((d & D_OK) == 0u) | (((d & D_NNCHK) != 0u) & (nn != (d >> 24)));
+  bool bad = oob | ((d & D_OK) == 0u) | (((d & D_YCHK) != 0u) & (y != (d >> 28)));
   bad |= is_ret & (L.sp == 0u);
   bad |= ((d & D_CALL) != 0u) & (L.sp == 16u);
   L.halted |= (uint32_t)(act & bad);
   act = act & !bad;
+  // ---- deferred DXYN: resolve the queues before anything that observes their effect:
+  //      a read of VF while a queued draw still owns it, CLS, a RAM write (sprite bytes),
+  //      or a draw into a full queue
+  const uint32_t vx = VREG(x), vy = VREG(y);
   // ---- stack
   uint32_t ret_pc = 0;
   if (act & is_ret) ret_pc = sm.stk[(L.sp - 1u) * kBlock + tid];
@@ -367,9 +368,9 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     const uint32_t nrows = do_draw ? (((quirks & 8u) != 0u) ? n : min(n, 32u - y0)) : 0u;
     const uint32_t maxr = __reduce_max_sync(kFull, nrows);
     if (maxr <= kLaneDrawMax)
-      draw_lanes(sm, L, p, tid, do_draw, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks);
+      draw_lanes(sm, L, p, tid, do_draw, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
     else
-      draw_coop(sm, L, p, tid, lane, block0, do_draw, vx & 63u, y0, L.I & 0xFFFu, n);
+      draw_coop(sm, L, p, tid, lane, block0, do_draw, vx & 63u, y0, L.I & 0xFFFu, n, do_draw, quirks);
     __syncwarp();
   }
 }
@@ -598,6 +599,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       if (resetting) L.keys = p.startup_keys[seg];
       run_frames<Q0>(sm, L, p, tid, lane, block0, gid, resetting, p.startup_frames[seg], wdirty);
     }
+
     if (resetting) {
       L.keys = 0;
       steps = 0;
