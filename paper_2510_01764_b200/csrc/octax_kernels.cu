@@ -685,28 +685,49 @@ __global__ void gen_actions_kernel(uint64_t n, uint64_t env_offset, uint64_t ase
   out[j] = (int32_t)(r % n_actions);
 }
 
-// packed [n][4][32][8] -> bool [n][4][64][32]; one thread writes 16 bytes (16 y's of one x)
-__global__ void expand_obs_kernel(uint64_t n, const uint8_t *__restrict__ packed, uint8_t *__restrict__ dense,
-                                  const uint8_t *__restrict__ row_mask) {
-  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;  // unit of 16 output bytes
-  uint64_t total = n * 4 * 64 * 2;
-  if (i >= total) return;
-  if (row_mask && !row_mask[i >> 9]) return;  // 512 units of 16 B per env
-  uint32_t yh = i & 1, x = (i >> 1) & 63;
-  uint64_t plane = i >> 7;  // env*4 + p
-  const uint8_t *src = packed + plane * 256;
-  uint32_t w[4];
+// packed [n][4][32][8] -> bool [n][4][64][32] (P:146 axis order [frame][x][y]).
+// One warp per plane: lane y loads row y, the two 32x32 bit blocks (x = 0..31,
+// 32..63) are transposed across the warp with 5 shuffle-xor stages each, so lane
+// x then holds column x (bit y = pixel (x, y)); each column's 32 bits are spread
+// to 32 bytes (nibble * 0x204081 & 0x01010101 puts 4 bits into 4 bytes) and
+// stored as two 16-byte vectors -- coalesced 2 KB per plane.
+__device__ __forceinline__ uint32_t transpose32(uint32_t w, int lane) {
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint32_t acc = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint32_t y = yh * 16 + q * 4 + k;
-      acc |= ((uint32_t)(src[y * 8 + (x >> 3)] >> (7 - (x & 7))) & 1u) << (8 * k);
-    }
-    w[q] = acc;
+  for (int s = 0; s < 5; ++s) {
+    const int j = 16 >> s;
+    const uint32_t lo = masks[s];
+    const uint32_t t = __shfl_xor_sync(kFull, w, j);
+    w = (lane & j) ? ((w & ~lo) | ((t >> j) & lo)) : ((w & lo) | ((t << j) & ~lo));
   }
-  reinterpret_cast<uint4 *>(dense)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+  return w;
+}
+
+__device__ __forceinline__ uint4 spread8(uint32_t bits16, int half) {
+  uint32_t v[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) v[q] = (((bits16 >> (16 * half + 4 * q)) & 15u) * 0x204081u) & 0x01010101u;
+  return make_uint4(v[0], v[1], v[2], v[3]);
+}
+
+__global__ void __launch_bounds__(256) expand_obs_kernel(uint64_t n, const uint8_t *__restrict__ packed,
+                                                         uint8_t *__restrict__ dense,
+                                                         const uint8_t *__restrict__ row_mask) {
+  const uint64_t plane = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (plane >= n * 4) return;                       // uniform per warp
+  if (row_mask && !row_mask[plane >> 2]) return;    // uniform per warp
+  const uint64_t row = reinterpret_cast<const uint64_t *>(packed)[plane * 32 + lane];
+  // bit x of nat_lo / nat_hi = pixel x / 32 + x (packed bytes are MSB-first)
+  const uint32_t nat_lo = __byte_perm(__brev((uint32_t)row), 0, 0x0123);
+  const uint32_t nat_hi = __byte_perm(__brev((uint32_t)(row >> 32)), 0, 0x0123);
+  const uint32_t col_lo = transpose32(nat_lo, lane);  // column x = lane
+  const uint32_t col_hi = transpose32(nat_hi, lane);  // column x = 32 + lane
+  uint4 *out = reinterpret_cast<uint4 *>(dense + plane * 2048);
+  out[lane * 2] = spread8(col_lo, 0);
+  out[lane * 2 + 1] = spread8(col_lo, 1);
+  out[64 + lane * 2] = spread8(col_hi, 0);
+  out[64 + lane * 2 + 1] = spread8(col_hi, 1);
 }
 
 // canonical per-env state (DESIGN.md layout), one CTA of 128 threads per requested env
@@ -808,8 +829,8 @@ cudaError_t launch_gen_actions(uint64_t n, uint64_t env_offset, uint64_t aseed, 
 
 cudaError_t launch_expand_obs(uint64_t n, const uint8_t *packed, uint8_t *dense, cudaStream_t stream,
                               const uint8_t *row_mask) {
-  uint64_t total = n * 4 * 64 * 2;
-  const unsigned grid = (unsigned)((total + 255) / 256);
+  const uint64_t threads = n * 4 * 32;  // one warp per plane
+  const unsigned grid = (unsigned)((threads + 255) / 256);
   expand_obs_kernel<<<grid, 256, 0, stream>>>(n, packed, dense, row_mask);
   return cudaGetLastError();
 }

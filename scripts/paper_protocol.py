@@ -1,0 +1,109 @@
+#!/usr/bin/env python
+"""The paper's throughput protocol ("execution time for 100-step rollouts ...
+with 50 independent measurements per configuration"; steps/s = envs x 100 / time),
+run on the BASELINE.json configurations, plus the CPU oracle on the same box.
+
+    python scripts/paper_protocol.py [--reps 50] [--out profiles/r01_paper_protocol]
+
+Writes <out>.json and <out>.md (median and IQR of the 50 rollouts).  Each
+rollout = 100 octax_step launches with device-resident, pre-generated actions,
+timed with CUDA events on the env's stream after one untimed warm-up rollout.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import workloads  # noqa: E402
+from paper_2510_01764_b200 import OctaxEnv  # noqa: E402
+
+CONFIGS = [
+    # (config id, game, envs, obs_format, action mode)
+    ("1", "coverage", 1, 0, "random"),
+    ("2", "pong_standin", 4096, 0, "random"),
+    ("2", "pong_standin", 4096, 0, "constant"),
+    ("2*", "pong_standin", 8192, 0, "constant"),          # the paper's 350K steps/s point
+    ("3", "brix_standin", 65536, 0, "random"),
+    ("3", "brix_standin", 65536, 1, "random"),
+    ("4", "pong_standin", 262144, 0, "random"),
+    ("4", "brix_standin", 262144, 0, "random"),
+    ("4", "target_shooter_level1", 262144, 0, "random"),
+    ("4", "target_shooter_level2", 262144, 0, "random"),
+    ("4", "target_shooter_level3", 262144, 0, "random"),
+] + [("5", g, n, 0, "random") for g in ("pong_standin", "target_shooter_level3")
+     for n in (1024, 4096, 16384, 65536, 262144, 1048576)]
+
+
+def rollouts(game, n, obs_format, mode, reps, T=100):
+    rom, spec = workloads.game(game, obs_format=obs_format)
+    s = torch.cuda.Stream()
+    env = OctaxEnv(rom, spec, n, workloads.ENV_SEED, stream=s)
+    acts = torch.zeros((T, n), dtype=torch.int32, device="cuda")
+    if mode == "random":
+        with torch.cuda.stream(s):
+            for t in range(T):
+                env.gen_actions(workloads.ACTION_SEED, t, acts[t])
+    s.synchronize()
+    obs, rew, done = env.obs, env.reward, env.done
+    times = []
+    for r in range(reps + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for t in range(T):
+            env.step_into(acts[t], obs, rew, done)
+        e1.record(s)
+        e1.synchronize()
+        if r > 0:  # first rollout is the warm-up
+            times.append(e0.elapsed_time(e1) / 1e3)
+    env.close()
+    sps = np.array([n * T / t for t in times])
+    return float(np.median(sps)), float(np.percentile(sps, 75) - np.percentile(sps, 25))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_paper_protocol"))
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    import bench
+    rows = []
+    cpu_cache = {}
+    for cid, game, n, fmt, mode in CONFIGS:
+        med, iqr = rollouts(game, n, fmt, mode, args.reps)
+        row = {"config": cid, "game": game, "envs": n, "obs": "bool" if fmt else "packed", "actions": mode,
+               "steps_per_s_median": med, "steps_per_s_iqr": iqr, "frames_per_s_median": 4 * med}
+        if not args.no_cpu and game not in cpu_cache:
+            one, _, _ = bench.oracle_throughput(game, 256, 100, procs=1)
+            allc, C, _ = bench.oracle_throughput(game, 256, 100)
+            cpu_cache[game] = (one[0], allc[0], C)
+        if game in cpu_cache:
+            row["oracle_1core"], row["oracle_all_cores"], row["cores"] = cpu_cache[game]
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+    dev = torch.cuda.get_device_name(0)
+    with open(args.out + ".json", "w") as f:
+        json.dump({"device": dev, "protocol": "P:228, 1 warm-up + %d x 100-step rollouts" % args.reps,
+                   "rows": rows}, f, indent=1)
+    lines = ["| config | game | envs | obs | actions | steps/s median | IQR | frames/s | oracle 1 core | oracle all cores (C) |",
+             "|---|---|---|---|---|---|---|---|---|---|"]
+    for r in rows:
+        lines.append(f"| {r['config']} | {r['game']} | {r['envs']:,} | {r['obs']} | {r['actions']} | "
+                     f"{r['steps_per_s_median']:.4g} | {r['steps_per_s_iqr']:.3g} | {r['frames_per_s_median']:.4g} | "
+                     f"{r.get('oracle_1core', float('nan')):.3g} | {r.get('oracle_all_cores', float('nan')):.3g} ({r.get('cores', '-')}) |")
+    with open(args.out + ".md", "w") as f:
+        f.write(f"# Paper protocol (P:228) on {dev}\n\n1 warm-up + {args.reps} timed 100-step rollouts per row; "
+                "CUDA events; device-resident actions.\n\n" + "\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
