@@ -9,6 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "liboctax.so")
+SO_CHECKED = os.path.join(HERE, "liboctax_checked.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("octax_kernels.cu", "octax_api.cpp")]
 HEADERS = [os.path.join(CSRC, "octax_dev.cuh"), os.path.join(ROOT, "include", "octax.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -22,29 +23,30 @@ FLAGS = [
 ]
 
 
-def stale() -> bool:
-    if not os.path.exists(SO):
+def stale(so: str = SO) -> bool:
+    if not os.path.exists(so):
         return True
-    t = os.path.getmtime(SO)
+    t = os.path.getmtime(so)
     return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
-        return SO
-    cmd = [NVCC, *FLAGS, "-o", SO, *SOURCES]
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """liboctax.so (release) or liboctax_checked.so (-DOCTAX_CHECKS device bounds asserts)."""
+    so = SO_CHECKED if checked else SO
+    if not force and not stale(so):
+        return so
+    cmd = [NVCC, *FLAGS, *(["-DOCTAX_CHECKS"] if checked else []), "-o", so, *SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = r.stdout + r.stderr
-    with open(os.path.join(HERE, "build.log"), "w") as f:
+    with open(os.path.join(HERE, "build_checked.log" if checked else "build.log"), "w") as f:
         f.write(" ".join(cmd) + "\n" + log)
     if r.returncode != 0:
         sys.stderr.write(log)
-        raise RuntimeError("nvcc failed building liboctax.so")
+        raise RuntimeError(f"nvcc failed building {os.path.basename(so)}")
     if verbose:
         sys.stderr.write(log)
-    return SO
+    return so
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(SO)
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

@@ -26,9 +26,19 @@
 // the CPU oracle in oracle/.
 #include <cuda_runtime.h>
 
+#include <cassert>
 #include <cstdint>
 
 #include "octax_dev.cuh"
+
+// Checked build (liboctax_checked.so, -DOCTAX_CHECKS): device-side bounds asserts on
+// every computed shared / global index -- the substitute for compute-sanitizer, which
+// is closed on this GPU pool.
+#ifdef OCTAX_CHECKS
+#define OCTAX_CHECK(c) assert(c)
+#else
+#define OCTAX_CHECK(c) ((void)0)
+#endif
 
 namespace octax {
 
@@ -50,7 +60,10 @@ struct __align__(128) Smem {
 size_t smem_bytes() { return sizeof(Smem); }
 
 // framebuffer row `r` of CTA-local env `e`: XOR swizzle on the low 4 row bits
-__device__ __forceinline__ uint32_t fb_idx(uint32_t e, uint32_t r) { return e * 32u + (r ^ (e & 15u)); }
+__device__ __forceinline__ uint32_t fb_idx(uint32_t e, uint32_t r) {
+  OCTAX_CHECK(e < (uint32_t)kBlock && r < 32u);
+  return e * 32u + (r ^ (e & 15u));
+}
 
 __device__ __forceinline__ uint64_t bswap64(uint64_t v) {
   uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
@@ -109,10 +122,12 @@ struct Lane {
 #define VREG(k) sm.V[((k) << 7) + ((uint32_t)tid ^ ((uint32_t)(k) << 2))]
 
 __device__ __forceinline__ uint32_t rd(const Smem &sm, const Lane &L, uint32_t a) {
+  OCTAX_CHECK(a < 4096u);
   return ((L.dirty >> (a >> 6)) & 1ull) ? (uint32_t)L.ram[a] : (uint32_t)sm.img[a];
 }
 
 __device__ __forceinline__ void wr(const Smem &sm, Lane &L, uint32_t a, uint32_t v) {
+  OCTAX_CHECK(a < 4096u);
   uint32_t b = a >> 6;
   if (!((L.dirty >> b) & 1ull)) {  // copy-on-write: materialise the 64-B block
     const uint4 *src = reinterpret_cast<const uint4 *>(sm.img + b * 64);
@@ -274,6 +289,9 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   //      or a draw into a full queue
   const uint32_t vx = VREG(x), vy = VREG(y);
   // ---- stack
+  OCTAX_CHECK(!(act & is_ret) || (L.sp >= 1u && L.sp <= 16u));
+  OCTAX_CHECK(!(act & ((d & D_CALL) != 0u)) || L.sp < 16u);
+  OCTAX_CHECK(x < 16u && y < 16u && tid < kBlock);
   uint32_t ret_pc = 0;
   if (act & is_ret) ret_pc = sm.stk[(L.sp - 1u) * kBlock + tid];
   if (act & ((d & D_CALL) != 0u)) { sm.stk[L.sp * kBlock + tid] = (uint16_t)(pc + 2u); L.stk_dirty = 1; }
@@ -454,6 +472,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   const bool active = env < p.n;
   const uint64_t wbase = block0 + (uint64_t)warp * 32;
   const uint32_t h = p.head;
+  OCTAX_CHECK(h < 4u && blockDim.x == (unsigned)kBlock);
   uint64_t *__restrict__ ring = p.s.ring;
   uint64_t *__restrict__ obs64 = reinterpret_cast<uint64_t *>(obs);
   const int ne = p.n > wbase ? (int)((p.n - wbase) < 32 ? (p.n - wbase) : 32) : 0;

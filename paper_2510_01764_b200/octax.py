@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "liboctax.so")
+# OCTAX_CHECKED=1 selects the bounds-checked build (device asserts; tests / debugging)
+SO_PATH = os.path.join(_HERE, "liboctax_checked.so" if os.environ.get("OCTAX_CHECKED") == "1" else "liboctax.so")
 
 CANON_BYTES = 5200
 OBS_PACKED = 0

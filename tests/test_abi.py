@@ -37,6 +37,14 @@ def test_header_symbols_exported(lib):
     assert sorted(SYMBOLS) == names
 
 
+def test_checked_build_exports_same_symbols(lib):
+    from paper_2510_01764_b200 import build
+    so = build.build(checked=True)
+    L = ctypes.CDLL(so)
+    for n in _declared():
+        assert hasattr(L, n), n
+
+
 def test_sass_is_sm100a_with_bulk_copy(lib):
     so = os.path.join(ROOT, "paper_2510_01764_b200", "liboctax.so")
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", so], capture_output=True, text=True).stdout
