@@ -265,10 +265,10 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   bool act = part & (L.halted == 0u);
   const uint32_t pc = L.pc;
   const bool oob = pc > 0xFFEu;
-  // ---- fetch: one 8-byte load from the smem image (slow path: dirty block or straddle)
-  const uint64_t w8 = *reinterpret_cast<const uint64_t *>(sm.img + (pc & 0xFF8u));
-  uint32_t op = __byte_perm((uint32_t)(w8 >> ((pc & 7u) * 8u)), 0, 0x4401);
-  bool slow = act & !oob & ((pc & 7u) == 7u);
+  // ---- fetch: one aligned 16-bit load from the smem image (slow path: odd PC or dirty block)
+  const uint32_t w16 = *reinterpret_cast<const uint16_t *>(sm.img + (pc & 0xFFEu));
+  uint32_t op = __byte_perm(w16, 0, 0x4401);
+  bool slow = act & !oob & ((pc & 1u) != 0u);
   if (wdirty) slow |= act & !oob & (((L.dirty >> (pc >> 6)) & 1ull) != 0ull);
   if (__any_sync(kFull, slow)) {
     if (slow) op = (rd(sm, L, pc) << 8) | rd(sm, L, pc + 1);
@@ -346,15 +346,17 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     L.st = (d & D_STW) ? vx : L.st;
   }
   const bool f33 = nn == 0x33u, f55 = nn == 0x55u;  // only meaningful under D_MEM
-  // ---- vote-gated rare classes
+  // ---- vote-gated rare classes (one vote for CLS / CXNN / FX33-55-65 together)
   const bool do_cls = act & is_cls;
+  const bool do_rnd = act & ((d & D_RND) != 0u);
+  const bool do_mem = act & ((d & D_MEM) != 0u);
+  if (__any_sync(kFull, do_cls | do_rnd | do_mem)) {
   if (__any_sync(kFull, do_cls)) {
     if (do_cls) {
 #pragma unroll
       for (int r = 0; r < 32; ++r) sm.fb[tid * 32 + r] = 0;
     }
   }
-  const bool do_rnd = act & ((d & D_RND) != 0u);
   if (__any_sync(kFull, do_rnd)) {
     if (do_rnd) {
       const uint32_t r = philox_out0(L.draw, L.episode, gid, 0u, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
@@ -362,7 +364,6 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
       L.draw++;
     }
   }
-  const bool do_mem = act & ((d & D_MEM) != 0u);
   if (__any_sync(kFull, do_mem)) {
     if (do_mem) {
       if (f33) {
@@ -379,6 +380,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
       }
     }
     wdirty = __any_sync(kFull, L.dirty != 0ull);
+  }
   }
   const bool do_draw = act & ((d & D_DRAW) != 0u);
   if (__any_sync(kFull, do_draw)) {
