@@ -372,3 +372,20 @@ def test_vec_env_wrapper_shapes_and_values():
             fo = info["final_obs"].cpu().numpy().reshape(n, -1).astype(np.uint8)
             assert np.array_equal(fo[m], ofin[m])
             assert np.array_equal(info["episode"]["r"].cpu().numpy()[m], oer[m])
+
+
+EDGE_CASES = [(name, 0) for name in __import__("workloads.edge_roms", fromlist=["EDGE_ROMS"]).EDGE_ROMS] + \
+             [("draw_edges", 8), ("flags", 1 | 16), ("self_modify", 2)]
+
+
+@pytest.mark.parametrize("name,quirks", EDGE_CASES)
+def test_edge_rom_parity(name, quirks):
+    """SURVEY c.7 edge-case ROMs (self-modifying code, odd / boundary PCs, address
+    wrap, draw clipping / wrap / DXY0, X=Y=F flags, deep calls, key waits, timers,
+    RNG across resets), ragged n, bit-exact including full canonical state."""
+    from workloads import edge_roms
+    src, over = edge_roms.EDGE_ROMS[name]
+    spec = dict(workloads.DEFAULTS, score="V6 + (V1 << 8) + mem[0x300]", terminated="0",
+                action_keys=list(range(16)), max_episode_steps=150, quirks=quirks)
+    spec.update(over)
+    _run_parity(edge_roms.rom(name), spec, 97, 160, 11 + quirks, 7, check_every=16)
