@@ -78,7 +78,12 @@ enum {
   OCTAX_Q_VF_RESET = 16         /* 8XY1/2/3 clear VF                          */
 };
 
-enum { OCTAX_OBS_PACKED = 0, OCTAX_OBS_BOOL_XMAJOR = 1 };
+enum { OCTAX_OBS_PACKED = 0, OCTAX_OBS_BOOL_XMAJOR = 1,
+       /* flag, OR-ed with a layout: stack the displays after the last 4 FRAMES of the step
+          (the other reading of P:146 "4-frame stacking") instead of the last
+          4 step-end displays (A3, default); with frame_skip < 4 the missing leading planes
+          repeat the step-start display; reset obs = 4 copies of the reset display */
+       OCTAX_OBS_STACK_FRAMES = 16 };
 
 #define OCTAX_MAX_STARTUP 32u   /* startup segments per spec                   */
 #define OCTAX_MAX_EXPR_OPS 64u  /* compiled expression length (ops)            */
@@ -106,7 +111,8 @@ typedef struct {
   uint32_t instructions_per_frame;   /* >= 1, default 12 (A1)                        */
   uint32_t max_episode_steps;        /* 0 = no truncation, default 10000 (A9)        */
   uint32_t quirks;                   /* OCTAX_Q_* bits                               */
-  uint32_t obs_format;               /* OCTAX_OBS_*                                  */
+  uint32_t obs_format;               /* OCTAX_OBS_PACKED | OCTAX_OBS_BOOL_XMAJOR, optionally
+                                        | OCTAX_OBS_STACK_FRAMES                     */
 } octax_game_spec;
 
 /* Device placement.  env_offset / total_envs: this handle simulates global env

@@ -137,7 +137,7 @@ class OracleEnv:
         self.n = n_envs
         self.n_actions = len(spec.get("action_keys", [1])) + 1
         self.obs_format = spec.get("obs_format", OBS_PACKED)
-        self.obs_per_env = 1024 if self.obs_format == OBS_PACKED else 8192
+        self.obs_per_env = 1024 if (self.obs_format & 1) == OBS_PACKED else 8192
         cs, keep = _make_spec(spec)
         rom_arr = (ctypes.c_uint8 * max(1, len(rom)))(*rom)
         h = ctypes.c_void_p()

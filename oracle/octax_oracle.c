@@ -393,6 +393,7 @@ typedef struct {
   uint32_t episode, draw, steps, prev_score;
   int32_t ep_ret;
   bool hist[4][H][W]; /* oldest .. newest; hist[3] == disp between steps */
+  bool fr[4][H][W];   /* OBS_STACK_FRAMES: displays after the last 4 frames of the step */
   uint64_t gid;
   uint64_t cls_count[16]; /* workload trace: cycles by op>>12 */
   uint64_t rows_drawn;
@@ -658,18 +659,21 @@ static void env_reset_one(const oracle_env *e, vm *m) {
   m->steps = 0;
   m->prev_score = eval_node(e->score, m);
   for (int p = 0; p < 4; p++) memcpy(m->hist[p], m->disp, sizeof m->disp);
+  for (int p = 0; p < 4; p++) memcpy(m->fr[p], m->disp, sizeof m->disp);
   m->ep_ret = 0;
 }
 
 static void write_obs(const oracle_env *e, const vm *m, uint8_t *obs_env) {
-  if (e->obs_format == ORACLE_OBS_PACKED) {
+  /* A3 default: the last 4 step-end displays; OBS_STACK_FRAMES: the last 4 frames */
+  const bool(*src)[H][W] = (e->obs_format & ORACLE_OBS_STACK_FRAMES) ? m->fr : m->hist;
+  if ((e->obs_format & 1u) == ORACLE_OBS_PACKED) {
     /* obs[p][y][b] = sum_c hist[p][y][8b+c] << (7-c) */
     for (int p = 0; p < 4; p++)
       for (int y = 0; y < H; y++)
         for (int b = 0; b < 8; b++) {
           uint8_t v = 0;
           for (int c = 0; c < 8; c++)
-            if (m->hist[p][y][8 * b + c]) v |= (uint8_t)(1u << (7 - c));
+            if (src[p][y][8 * b + c]) v |= (uint8_t)(1u << (7 - c));
           obs_env[(p * H + y) * 8 + b] = v;
         }
   } else {
@@ -677,12 +681,12 @@ static void write_obs(const oracle_env *e, const vm *m, uint8_t *obs_env) {
     for (int p = 0; p < 4; p++)
       for (int x = 0; x < W; x++)
         for (int y = 0; y < H; y++)
-          obs_env[(p * W + x) * H + y] = m->hist[p][y][x] ? 1 : 0;
+          obs_env[(p * W + x) * H + y] = src[p][y][x] ? 1 : 0;
   }
 }
 
 static size_t obs_bytes(const oracle_env *e) {
-  return e->obs_format == ORACLE_OBS_PACKED ? 4u * 32u * 8u : 4u * 64u * 32u;
+  return (e->obs_format & 1u) == ORACLE_OBS_PACKED ? 4u * 32u * 8u : 4u * 64u * 32u;
 }
 
 /* ------------------------------------------------------------------ */
@@ -719,7 +723,7 @@ int octax_oracle_create(const uint8_t *rom, size_t rom_len,
   }
   if (spec->n_startup > 0 && !spec->startup) return fail(ORACLE_E_SPEC, "startup is NULL");
   if (spec->quirks & ~31u) return fail(ORACLE_E_SPEC, "unknown quirk bits");
-  if (spec->obs_format > 1) return fail(ORACLE_E_SPEC, "unknown obs_format");
+  if (spec->obs_format & ~(1u | ORACLE_OBS_STACK_FRAMES)) return fail(ORACLE_E_SPEC, "unknown obs_format");
   if (!spec->score_expr || !spec->terminated_expr)
     return fail(ORACLE_E_SPEC, "expressions must be non-NULL");
 
@@ -800,7 +804,13 @@ int octax_oracle_step_ex(oracle_env *e, const int32_t *actions, uint8_t *obs_out
       a = 0;
     }
     m->keys = a == 0 ? 0 : (uint16_t)(1u << e->action_keys[a - 1]); /* A5 */
-    for (uint32_t f = 0; f < e->frame_skip; f++) frame(e, m);
+    for (int p = 0; p < 4; p++) memcpy(m->fr[p], m->disp, sizeof m->disp);
+    for (uint32_t f = 0; f < e->frame_skip; f++) {
+      frame(e, m);
+      /* frame f is plane f + 4 - frame_skip of the intra-step stack (when >= 0) */
+      long pl = (long)f + 4 - (long)e->frame_skip;
+      if (pl >= 0) memcpy(m->fr[pl], m->disp, sizeof m->disp);
+    }
     uint32_t s = eval_node(e->score, m);
     int32_t d = (int32_t)(s - m->prev_score); /* A6, A7: signed delta */
     float reward = (float)d;

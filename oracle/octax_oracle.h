@@ -50,6 +50,7 @@ extern "C" {
 /* observation formats (A3, A4) */
 #define ORACLE_OBS_PACKED 0u      /* u8 [n][4][32][8], MSB = leftmost pixel */
 #define ORACLE_OBS_BOOL_XMAJOR 1u /* u8 0/1 [n][4][64][32], paper axis order */
+#define ORACLE_OBS_STACK_FRAMES 16u /* flag: stack the last 4 frames of the step */
 
 #define ORACLE_CANON_BYTES 5200u
 

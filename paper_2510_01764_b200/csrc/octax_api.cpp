@@ -419,7 +419,7 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   if (spec->n_startup > kMaxStartup) return set_err(OCTAX_E_SPEC, "more than %u startup segments", kMaxStartup);
   if (spec->n_startup && !spec->startup) return set_err(OCTAX_E_SPEC, "startup is NULL");
   if (spec->quirks & ~31u) return set_err(OCTAX_E_SPEC, "unknown quirk bits");
-  if (spec->obs_format > 1) return set_err(OCTAX_E_SPEC, "unknown obs_format");
+  if (spec->obs_format & ~(uint32_t)(1 | OCTAX_OBS_STACK_FRAMES)) return set_err(OCTAX_E_SPEC, "unknown obs_format");
 
   octax_env *e = new octax_env();
   StepParams &p = e->p;
@@ -432,8 +432,8 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   e->n = n_envs;
   e->env_offset = opts ? opts->env_offset : 0;
   e->total = (opts && opts->total_envs) ? opts->total_envs : n_envs;
-  e->obs_format = spec->obs_format;
-  e->obs_bytes = spec->obs_format == OCTAX_OBS_PACKED ? 1024 : 8192;
+  e->obs_format = spec->obs_format & 1u;  // layout; the stacking flag goes to the kernel
+  e->obs_bytes = e->obs_format == OCTAX_OBS_PACKED ? 1024 : 8192;
 
   p.n = n_envs;
   p.env_offset = e->env_offset;
@@ -441,7 +441,8 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   p.ipf = spec->instructions_per_frame;
   p.max_steps = spec->max_episode_steps;
   p.quirks = spec->quirks;
-  p.obs_format = spec->obs_format;
+  p.obs_format = spec->obs_format & 1u;
+  p.stack_frames = (spec->obs_format & OCTAX_OBS_STACK_FRAMES) ? 1u : 0u;
   p.n_actions = spec->n_action_keys + 1;
   p.keymask[0] = 0;
   for (uint32_t k = 0; k < spec->n_action_keys; ++k) p.keymask[k + 1] = (uint16_t)(1u << spec->action_keys[k]);

@@ -88,6 +88,7 @@ struct StepParams {
   uint32_t max_steps;
   uint32_t quirks;
   uint32_t obs_format;
+  uint32_t stack_frames;  // OCTAX_OBS_STACK_FRAMES: obs = last 4 frames of the step
   uint32_t n_actions;     // n_action_keys + 1
   uint32_t n_startup;
   uint16_t keymask[17];   // action -> key mask

@@ -530,16 +530,25 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   long long ret_acc = 0;
   bool resetting;
   if (MODE == MODE_STEP) {
-    // obs plane 2 = display at the start of the step (from smem, before any draw)
-    for (int e = 0; e < ne; ++e) obs64[(wbase + e) * 128 + 64 + lane] = sm.fb[fb_idx(warp * 32 + e, lane)];
+    // Stacking (A3): by default obs = the last 4 step-END displays -- planes 0,1 come from
+    // the ring (copied one env per VM cycle: loads before the cycle, stores after it, so
+    // the HBM latency hides behind it), plane 2 = the step-start display.  With
+    // stack_frames (OCTAX_OBS_STACK_FRAMES) obs = the displays after the last 4 FRAMES of
+    // this step; planes for frames before the step (frame_skip < 4) = step-start display.
+    const bool sf = p.stack_frames != 0u;
+    const int first = sf ? 4 - (int)p.frame_skip : 3;  // planes [0, first) <- step-start display
+    for (int e = 0; e < ne; ++e) {
+      const uint64_t v = sm.fb[fb_idx(warp * 32 + e, lane)];
+      uint64_t *ob = obs64 + (wbase + e) * 128;
+      if (!sf) ob[64 + lane] = v;
+      for (int pl = 0; pl < first && pl < 3 && sf; ++pl) ob[pl * 32 + lane] = v;
+    }
     if (active) {
       int32_t a = actions[env];
       if (a < 0 || (uint32_t)a >= p.n_actions) { err = 1; a = 0; }
       L.keys = p.keymask[a];
     }
-    // frame loop; env `cur` of this warp gets its obs planes 0,1 copied per VM cycle:
-    // loads issued before the cycle, stores after it, so HBM latency hides behind it
-    int cur = 0;
+    int cur = sf ? ne : 0;
     for (uint32_t f = 0; f < p.frame_skip; ++f) {
       for (uint32_t k = 0; k < p.ipf; ++k) {
         const bool cp = cur < ne;
@@ -560,6 +569,12 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       if (active && !L.halted) {
         L.dt -= (L.dt != 0u);
         L.st -= (L.st != 0u);
+      }
+      const int pl = (int)f + 4 - (int)p.frame_skip;  // obs plane of this frame (stack_frames)
+      if (sf && pl >= 0 && pl < 3) {
+        __syncwarp();
+        for (int e = 0; e < ne; ++e)
+          obs64[(wbase + e) * 128 + pl * 32 + lane] = sm.fb[fb_idx(warp * 32 + e, lane)];
       }
     }
 #pragma unroll 4
@@ -598,10 +613,11 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
         const int e = __ffs(dm) - 1;
         dm &= dm - 1;
         const uint64_t *rg = ring + (wbase + e) * 128;
+        const uint64_t *ob = obs64 + (wbase + e) * 128;  // this step's frames (stack_frames)
         uint64_t *fo = fo64 + (wbase + e) * 128;
-        fo[lane] = rg[s0 * 32 + lane];
-        fo[32 + lane] = rg[s1 * 32 + lane];
-        fo[64 + lane] = rg[s2 * 32 + lane];
+        fo[lane] = sf ? ob[lane] : rg[s0 * 32 + lane];
+        fo[32 + lane] = sf ? ob[32 + lane] : rg[s1 * 32 + lane];
+        fo[64 + lane] = sf ? ob[64 + lane] : rg[s2 * 32 + lane];
         fo[96 + lane] = sm.fb[fb_idx(warp * 32 + e, lane)];
       }
       __syncwarp();

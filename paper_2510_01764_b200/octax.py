@@ -18,6 +18,7 @@ SO_PATH = os.path.join(_HERE, "liboctax_checked.so" if os.environ.get("OCTAX_CHE
 CANON_BYTES = 5200
 OBS_PACKED = 0
 OBS_BOOL_XMAJOR = 1
+OBS_STACK_FRAMES = 16
 
 # every symbol include/octax.h declares
 SYMBOLS = (
@@ -154,7 +155,7 @@ class OctaxEnv:
         self.n = int(n_envs)
         self.spec = dict(spec)
         self.n_actions = len(spec["action_keys"]) + 1
-        self.obs_format = spec.get("obs_format", OBS_PACKED)
+        self.obs_format = spec.get("obs_format", OBS_PACKED) & 1
         self.obs_per_env = 1024 if self.obs_format == OBS_PACKED else 8192
         cs, self._keep = _make_spec(spec)
         rom_arr = (ctypes.c_uint8 * max(1, len(rom)))(*rom)

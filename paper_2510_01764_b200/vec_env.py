@@ -14,6 +14,9 @@ C ABI -- argument marshalling only, every step runs in liboctax.so:
   episodes' return ``r`` and length ``l`` (valid where ``info["episode"]["_r"]``).
 * observations are torch CUDA tensors: bool ``[n, 4, 64, 32]`` (P:146 axis order)
   when ``dense=True``, else the packed ``[n, 4, 32, 8]`` uint8 form.
+* ``stack="steps"`` (default, reading A3): the 4 planes are the last 4 step-end
+  displays; ``stack="frames"``: the displays after the last 4 emulated frames of
+  the step (OCTAX_OBS_STACK_FRAMES).
 Gymnasium itself is not a dependency; ``single_observation_space`` /
 ``single_action_space`` are plain descriptors with ``shape`` / ``n``.
 """
@@ -21,7 +24,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from .octax import OBS_BOOL_XMAJOR, OBS_PACKED, OctaxEnv
+from .octax import OBS_BOOL_XMAJOR, OBS_PACKED, OBS_STACK_FRAMES, OctaxEnv
 
 
 @dataclass(frozen=True)
@@ -39,9 +42,12 @@ class Discrete:
 
 class OctaxVecEnv:
     def __init__(self, rom: bytes, spec: dict, num_envs: int, seed: int = 0, device: int = 0,
-                 dense: bool = True, env_offset: int = 0, stream=None):
+                 dense: bool = True, env_offset: int = 0, stream=None, stack: str = "steps"):
         import torch
-        spec = dict(spec, obs_format=OBS_BOOL_XMAJOR if dense else OBS_PACKED)
+        if stack not in ("steps", "frames"):
+            raise ValueError(f"stack must be 'steps' or 'frames', got {stack!r}")
+        fmt = (OBS_BOOL_XMAJOR if dense else OBS_PACKED) | (OBS_STACK_FRAMES if stack == "frames" else 0)
+        spec = dict(spec, obs_format=fmt)
         self._env = OctaxEnv(rom, spec, num_envs, seed, device=device, env_offset=env_offset, stream=stream)
         self.num_envs = num_envs
         self.dense = dense

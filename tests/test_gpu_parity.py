@@ -349,6 +349,31 @@ def test_step_ex_final_obs_and_episode_info(obs_format):
     assert seen > 20
 
 
+@pytest.mark.parametrize("obs_format,fs", [(16, 4), (16, 1), (16, 2), (16, 6), (17, 4), (17, 3)])
+def test_stack_frames_obs_parity(obs_format, fs):
+    """OCTAX_OBS_STACK_FRAMES: obs = the displays after the last 4 frames of the step
+    (per-frame smem->HBM stores inside the kernel), incl. terminal final_obs and
+    same-step resets, bit-exact vs the oracle."""
+    rom, spec = workloads.game("brix_standin", obs_format=obs_format, frame_skip=fs, max_episode_steps=33)
+    n = 291
+    g = _gpu_env(rom, spec, n, 17)
+    o = oracle.OracleEnv(rom, spec, n, 17)
+    fin = torch.zeros(n * g.obs_per_env, dtype=torch.uint8, device="cuda")
+    seen = 0
+    for t in range(80):
+        acts = workloads.gen.actions(5, t, n, 3)
+        g.step_ex(torch.from_numpy(acts).cuda(), final_obs=fin)
+        oo, orw, od, ot, otr, ofin, oer, oel = o.step_ex(acts)
+        assert np.array_equal(g.obs.cpu().numpy().reshape(n, -1), oo), t
+        assert np.array_equal(g.reward.cpu().numpy(), orw), t
+        d = od.astype(bool)
+        if d.any():
+            assert np.array_equal(fin.cpu().numpy().reshape(n, -1)[d], ofin[d]), t
+            seen += int(d.sum())
+    _assert_states(g, o, list(range(0, n, 7)))
+    assert seen > 0
+
+
 def test_vec_env_wrapper_shapes_and_values():
     from paper_2510_01764_b200.vec_env import OctaxVecEnv
     rom, spec = workloads.game("brix_standin", max_episode_steps=30)

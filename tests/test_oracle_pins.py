@@ -500,3 +500,47 @@ def test_coverage_rom_self_checks_pass():
     assert f["mem"][0xF00] == n_groups == 20
     assert np.all(f["mem"][0xF01:0xF01 + n_groups] == 0xA5)
     assert total == n_groups                        # telescoping: score went 0 -> 20
+
+
+# ---------------------------------------------------------------- intra-step frame stacking
+@pytest.mark.parametrize("fs", [1, 2, 4, 6])
+@pytest.mark.parametrize("game", ["pong_standin", "target_shooter_level1"])
+def test_stack_frames_equals_fs1_step_end_stack(game, fs):
+    """OBS_STACK_FRAMES (SPEC S:434 alternative) pinned to the default A3 stack of a
+    frame_skip=1 env holding each action for fs steps: frames [t*fs+1 .. (t+1)*fs]
+    are the last fs step-end displays there (planes before the step repeat the
+    step-start display when fs < 4)."""
+    rom, spec = workloads.game(game, terminated="0", max_episode_steps=0)
+    n = 6
+    a = oracle.OracleEnv(rom, dict(spec, frame_skip=fs, obs_format=16), n, 5)
+    b = oracle.OracleEnv(rom, dict(spec, frame_skip=1, obs_format=0), n, 5)
+    na = len(spec["action_keys"]) + 1
+    for t in range(25):
+        acts = workloads.gen.actions(3, t, n, na)
+        oa = a.step(acts)[0].reshape(n, 4, 32, 8)
+        for _ in range(fs):
+            ob = b.step(acts)[0].reshape(n, 4, 32, 8)
+        k = min(fs, 4)
+        assert np.array_equal(oa[:, 4 - k:], ob[:, 4 - k:])
+        for p in range(4 - k):                       # step-start display repeated
+            assert np.array_equal(oa[:, p], ob[:, 3 - k])
+
+
+def test_stack_frames_bool_layout_and_reset():
+    """Flag composes with the bool layout (bit 0); a terminal step's obs is the reset
+    display in all 4 planes; final_obs keeps the terminal step's frames."""
+    rom, spec = workloads.game("brix_standin", max_episode_steps=7)
+    n = 4
+    a = oracle.OracleEnv(rom, dict(spec, obs_format=17), n, 2)
+    p = oracle.OracleEnv(rom, dict(spec, obs_format=16), n, 2)
+    assert a.obs_per_env == 8192 and p.obs_per_env == 1024
+    for t in range(7):
+        acts = workloads.gen.actions(4, t, n, 3)
+        oa, _, da, _, _, fa, _, _ = a.step_ex(acts)
+        op, _, dp, _, _, fp, _, _ = p.step_ex(acts)
+        bits = oa.reshape(n, 4, 64, 32).transpose(0, 1, 3, 2)
+        assert np.array_equal(np.packbits(bits, axis=-1).reshape(n, -1), op)
+    assert da.all() and dp.all()
+    op4 = op.reshape(n, 4, 256)
+    assert all(np.array_equal(op4[:, 0], op4[:, q]) for q in range(1, 4))
+    assert not np.array_equal(fp.reshape(n, 4, 256)[:, 3], op4[:, 3])
