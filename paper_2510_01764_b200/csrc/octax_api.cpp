@@ -458,7 +458,8 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   size_t off = 0;
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
   size_t o_img = carve(kStageBytes), o_stats = carve(64), o_regs = carve(16 * n), o_ctrl = carve(16 * n),
-         o_book = carve(16 * n), o_stack = carve(32 * n), o_dirty = carve(8 * n), o_ring = carve(1024 * n),
+         o_book = carve(16 * n), o_stack = carve(32 * n), o_dirty = carve(8 * n),
+         o_ring = carve(1024 * ((n + kBlock - 1) / kBlock * kBlock)),
          o_ram = carve(4096 * n);
   e->block_bytes = off;
   cudaError_t ce = cudaMalloc(&e->block, off);
@@ -472,6 +473,7 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   p.s.stack = (uint4 *)(base + o_stack);
   p.s.dirty = (uint64_t *)(base + o_dirty);
   p.s.ring = (uint64_t *)(base + o_ring);
+  p.s.ring_stride = (n + kBlock - 1) / kBlock * kBlock * 32;
   p.s.ram = base + o_ram;
   // state is fully written by the reset kernel; zero the small fields anyway
   ce = cudaMemsetAsync(base, 0, o_ring, e->stream);

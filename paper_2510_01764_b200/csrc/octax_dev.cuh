@@ -68,7 +68,12 @@ struct DevState {
   uint4 *stack;      // [n*2]  16 x u16 return addresses
   uint64_t *dirty;   // [n]    copy-on-write block mask (64 blocks of 64 B)
   uint8_t *ram;      // [n*4096] RAM backing; only dirty blocks are valid
-  uint64_t *ring;    // [n][4][32] display history, packed byte order (bswap of row)
+  uint64_t *ring;    // [4][n_pad][32] display history, slot-major (n_pad = n rounded up to
+                     // kBlock, so a CTA's 128 envs are one contiguous 32 KB block per slot);
+                     // u64 = one row in packed byte order; position j of env e holds row
+                     // j ^ (e & 15) -- the shared-memory framebuffer's swizzle, so ring <->
+                     // smem moves are plain TMA bulk copies
+  uint64_t ring_stride;  // u64 per ring slot = n_pad * 32
   unsigned long long *stats;  // [4] {returns, episodes, steps, err}
   const uint8_t *image;       // [4096] pristine image: zeros, font at 0x50, ROM at 0x200
 };

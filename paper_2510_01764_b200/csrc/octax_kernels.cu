@@ -3,11 +3,12 @@
 // One thread = one environment (CHIP-8 VM), 128 envs per CTA.  Per step:
 //   * the 4 KB pristine image (font + ROM) is staged once per CTA into shared
 //     memory with a TMA bulk copy (cp.async.bulk + mbarrier);
-//   * a warp-cooperative prologue streams the three previous display planes
-//     of its 32 envs from the HBM ring straight into obs planes 0..2
-//     (coalesced 256 B per env-plane) and the newest one into the shared-memory
-//     framebuffer (32 x u64 rows per env, XOR-swizzled: bank-conflict free both
-//     for "one row of 32 envs" and "32 rows of one env" access);
+//   * the CTA's 32 KB block of the newest display slot of the HBM ring is staged
+//     into the shared-memory framebuffer with one more TMA bulk copy (32 x u64
+//     rows per env, XOR-swizzled: bank-conflict free both for "one row of 32 envs"
+//     and "32 rows of one env"; the ring keeps the same swizzle); obs planes 0..2
+//     are written in row order with 16-B lane chunks, planes 0,1 streamed from
+//     the ring one env per VM cycle behind the interpreter;
 //   * the interpreter loop (frame_skip x instructions_per_frame cycles,
 //     P:142-146) is WARP-UNIFORM: every lane runs the same straight-line,
 //     predicated core for the cheap opcode classes (no divergent dispatch
@@ -20,7 +21,8 @@
 //     gathered with one __reduce_or_sync;
 //   * score / termination bytecode -> reward, done; same-step
 //     auto-reset with startup segments (A10), also warp-uniform;
-//   * a warp-cooperative epilogue writes obs plane 3 and the new ring slot;
+//   * the epilogue bulk-stores the framebuffer block as the new ring slot and
+//     writes obs plane 3;
 //   * per-CTA integer episode statistics -> 4 int64 atomics per CTA.
 // Semantics follow DESIGN.md readings A1..A27; nothing here is shared with
 // the CPU oracle in oracle/.
@@ -84,22 +86,31 @@ __device__ __forceinline__ uint32_t philox_out0(uint32_t c0, uint32_t c1, uint32
   return c0;
 }
 
-// ---------------------------------------------------------------- TMA image load
-__device__ __forceinline__ void image_load_issue(Smem &sm, const uint8_t *src) {
+// ---------------------------------------------------------------- TMA bulk copies
+// One elected thread stages the 5 KB image (+ decode table) and, in a step, the CTA's
+// 32 KB framebuffer block of ring slot `h` into shared memory on one mbarrier.
+__device__ __forceinline__ void stage_issue(Smem &sm, const uint8_t *img, const uint64_t *fb_src) {
   uint32_t bar = (uint32_t)__cvta_generic_to_shared(&sm.bar);
   uint32_t dst = (uint32_t)__cvta_generic_to_shared(sm.img);
+  const uint32_t bytes = kStageBytes + (fb_src ? (uint32_t)sizeof(sm.fb) : 0u);
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kStageBytes)
-               : "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-      "l"(src), "r"(kStageBytes), "r"(bar)
+      "l"(img), "r"(kStageBytes), "r"(bar)
       : "memory");
+  if (fb_src) {
+    const uint32_t fdst = (uint32_t)__cvta_generic_to_shared(sm.fb);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(fdst),
+        "l"(fb_src), "r"((uint32_t)sizeof(sm.fb)), "r"(bar)
+        : "memory");
+  }
 }
 
-__device__ __forceinline__ void image_load_wait(Smem &sm) {
+__device__ __forceinline__ void stage_wait(Smem &sm) {
   uint32_t bar = (uint32_t)__cvta_generic_to_shared(&sm.bar);
   uint32_t done = 0;
   while (!done) {
@@ -109,6 +120,26 @@ __device__ __forceinline__ void image_load_wait(Smem &sm) {
         : "r"(bar)
         : "memory");
   }
+}
+
+// CTA framebuffer block -> one ring slot (bulk store; caller fenced + synced the CTA)
+__device__ __forceinline__ void fb_store_issue(const Smem &sm, uint64_t *dst) {
+  const uint32_t src = (uint32_t)__cvta_generic_to_shared(sm.fb);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+               "r"((uint32_t)sizeof(sm.fb))
+               : "memory");
+}
+
+// ring slot `slot` of handle-local env `e` (32 positions; position j holds row j ^ (e & 15))
+__device__ __forceinline__ uint64_t *ring_at(const StepParams &p, uint32_t slot, uint64_t e) {
+  return p.s.ring + (uint64_t)slot * p.s.ring_stride + e * 32u;
+}
+
+// obs plane `pl` of a pair of envs from 16-B chunks in position order: lanes 0-15 serve
+// env e, 16-31 env e+1; chunk 2l..2l+1 holds rows ra, ra^1 with ra = 2l ^ (e & 15).
+__device__ __forceinline__ void put_rows(uint64_t *ob_env, uint32_t pl, uint32_t ra, uint4 q) {
+  __stcs(ob_env + pl * 32u + ra, ((uint64_t)q.y << 32) | q.x);
+  __stcs(ob_env + pl * 32u + (ra ^ 1u), ((uint64_t)q.w << 32) | q.z);
 }
 
 // ---------------------------------------------------------------- lane state
@@ -475,24 +506,14 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   const uint64_t wbase = block0 + (uint64_t)warp * 32;
   const uint32_t h = p.head;
   OCTAX_CHECK(h < 4u && blockDim.x == (unsigned)kBlock);
-  uint64_t *__restrict__ ring = p.s.ring;
   uint64_t *__restrict__ obs64 = reinterpret_cast<uint64_t *>(obs);
   const int ne = p.n > wbase ? (int)((p.n - wbase) < 32 ? (p.n - wbase) : 32) : 0;
-
-  if (tid == 0) image_load_issue(sm, p.s.image);
-
-  // ---- prologue: framebuffer <- ring[h] with asynchronous 8-byte copies (LDGSTS),
-  //      lane = row, no register round trip; obs planes 0..2 are copied later,
-  //      pipelined behind the interpreter (see the frame loop).
   const uint32_t s0 = (h + 2) & 3, s1 = (h + 3) & 3, s2 = h & 3;
-  if (MODE == MODE_STEP) {
-    for (int e = 0; e < ne; ++e) {
-      const uint64_t *src = ring + (wbase + e) * 128 + s2 * 32 + lane;
-      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&sm.fb[fb_idx(warp * 32 + e, lane)]);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
+  const uint32_t hh = (uint32_t)lane >> 4, l2 = 2u * ((uint32_t)lane & 15u);  // 16-B chunk lanes
+
+  // ---- prologue: TMA bulk copies of the image and (step) the CTA's 32 KB framebuffer
+  //      block of ring slot h -- the ring keeps the smem swizzle, so no per-lane work
+  if (tid == 0) stage_issue(sm, p.s.image, MODE == MODE_STEP ? ring_at(p, s2, block0) : nullptr);
 
   Lane L;
   L.pc = 0x200; L.I = 0; L.sp = 0; L.dt = 0; L.st = 0; L.halted = 1; L.keys = 0; L.draw = 0; L.episode = 0;
@@ -518,11 +539,8 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     L.dirty = p.s.dirty[env];
     L.ram = p.s.ram + env * 4096ull;
   }
-  if (MODE == MODE_STEP) {
-    asm volatile("cp.async.wait_all;" ::: "memory");
-  }
-  __syncthreads();  // mbarrier init + framebuffer rows visible
-  image_load_wait(sm);
+  __syncthreads();  // mbarrier initialised
+  stage_wait(sm);
   bool wdirty = __any_sync(kFull, L.dirty != 0ull);  // any lane with private RAM blocks
 
   uint32_t done = 0, term = 0, trunc = 0, finished = 0, err = 0;
@@ -537,32 +555,38 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     // this step; planes for frames before the step (frame_skip < 4) = step-start display.
     const bool sf = p.stack_frames != 0u;
     const int first = sf ? 4 - (int)p.frame_skip : 3;  // planes [0, first) <- step-start display
-    for (int e = 0; e < ne; ++e) {
-      const uint64_t v = sm.fb[fb_idx(warp * 32 + e, lane)];
-      uint64_t *ob = obs64 + (wbase + e) * 128;
-      if (!sf) ob[64 + lane] = v;
-      for (int pl = 0; pl < first && pl < 3 && sf; ++pl) ob[pl * 32 + lane] = v;
+    if (!sf) {
+      for (int e = 0; e < ne; e += 2)  // plane 2 <- step-start display, two envs per pass
+        if (e + (int)hh < ne) {
+          const uint32_t el = (uint32_t)(warp * 32 + e) + hh;
+          const uint4 q = *reinterpret_cast<const uint4 *>(&sm.fb[el * 32u + l2]);
+          put_rows(obs64 + (wbase + e + hh) * 128, 2u, l2 ^ (el & 15u), q);
+        }
+    } else {
+      for (int e = 0; e < ne; ++e) {
+        const uint64_t v = sm.fb[fb_idx(warp * 32 + e, lane)];
+        uint64_t *ob = obs64 + (wbase + e) * 128;
+        for (int pl = 0; pl < first && pl < 3; ++pl) ob[pl * 32 + lane] = v;
+      }
     }
     if (active) {
       int32_t a = actions[env];
       if (a < 0 || (uint32_t)a >= p.n_actions) { err = 1; a = 0; }
       L.keys = p.keymask[a];
     }
+    // planes 0 (lanes 0-15, ring slot s0) and 1 (lanes 16-31, slot s1) of env `cur`:
+    // one 16-B chunk per lane, loaded before a cycle and stored (in row order) after it
+    const uint4 *rsrc = reinterpret_cast<const uint4 *>(ring_at(p, hh ? s1 : s0, wbase) + l2);
+    uint64_t *odst = obs64 + wbase * 128 + hh * 32;
     int cur = sf ? ne : 0;
     for (uint32_t f = 0; f < p.frame_skip; ++f) {
       for (uint32_t k = 0; k < p.ipf; ++k) {
         const bool cp = cur < ne;
-        uint64_t q0 = 0, q1 = 0;
-        if (cp) {
-          const uint64_t *rg = ring + (wbase + cur) * 128;
-          q0 = __ldcs(rg + s0 * 32 + lane);
-          q1 = __ldcs(rg + s1 * 32 + lane);
-        }
+        uint4 q = make_uint4(0, 0, 0, 0);
+        if (cp) q = __ldcs(rsrc + cur * 16);
         cycle<Q0>(sm, L, p, tid, lane, block0, gid, active, wdirty);
         if (cp) {
-          uint64_t *ob = obs64 + (wbase + cur) * 128;
-          __stcs(ob + lane, q0);
-          __stcs(ob + 32 + lane, q1);
+          put_rows(odst + cur * 128, 0u, l2 ^ ((uint32_t)cur & 15u), q);
           ++cur;
         }
       }
@@ -578,13 +602,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       }
     }
 #pragma unroll 4
-    for (int e = cur; e < ne; ++e) {
-      const uint64_t *rg = ring + (wbase + e) * 128;
-      uint64_t *ob = obs64 + (wbase + e) * 128;
-      const uint64_t q0 = __ldcs(rg + s0 * 32 + lane), q1 = __ldcs(rg + s1 * 32 + lane);
-      __stcs(ob + lane, q0);
-      __stcs(ob + 32 + lane, q1);
-    }
+    for (int e = cur; e < ne; ++e) put_rows(odst + e * 128, 0u, l2 ^ ((uint32_t)e & 15u), __ldcs(rsrc + e * 16));
     if (active) {
       const uint32_t s = eval(p.score, sm, L, tid);
       const int32_t d = (int32_t)(s - prev);
@@ -612,12 +630,11 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       while (dm) {
         const int e = __ffs(dm) - 1;
         dm &= dm - 1;
-        const uint64_t *rg = ring + (wbase + e) * 128;
-        const uint64_t *ob = obs64 + (wbase + e) * 128;  // this step's frames (stack_frames)
+        const uint64_t *ob = obs64 + (wbase + e) * 128;  // planes 0..2 already in obs
         uint64_t *fo = fo64 + (wbase + e) * 128;
-        fo[lane] = sf ? ob[lane] : rg[s0 * 32 + lane];
-        fo[32 + lane] = sf ? ob[32 + lane] : rg[s1 * 32 + lane];
-        fo[64 + lane] = sf ? ob[64 + lane] : rg[s2 * 32 + lane];
+        fo[lane] = ob[lane];
+        fo[32 + lane] = ob[32 + lane];
+        fo[64 + lane] = ob[64 + lane];
         fo[96 + lane] = sm.fb[fb_idx(warp * 32 + e, lane)];
       }
       __syncwarp();
@@ -646,26 +663,41 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   }
   __syncwarp();
 
-  // ---- warp-cooperative epilogue: new ring slot + obs plane 3 (all planes on reset)
-  {
-    const uint32_t sn = (h + 1) & 3;
-    for (int e = 0; e < ne; ++e) {
-      const uint64_t v = sm.fb[fb_idx(warp * 32 + e, lane)];
-      uint64_t *rg = ring + (wbase + e) * 128;
-      uint64_t *ob = obs64 ? obs64 + (wbase + e) * 128 : nullptr;
-      if (MODE == MODE_STEP) {
-        rg[sn * 32 + lane] = v;
-        ob[96 + lane] = v;
-        if ((reset_mask >> e) & 1u) {
-          rg[((h + 2) & 3) * 32 + lane] = v;
-          rg[((h + 3) & 3) * 32 + lane] = v;
-          rg[(h & 3) * 32 + lane] = v;
-          ob[lane] = v; ob[32 + lane] = v; ob[64 + lane] = v;
+  // ---- epilogue: the CTA's framebuffer block -> ring slot h+1 with one TMA bulk store
+  //      (all 4 slots on a reset launch); obs plane 3 in row order (all planes on reset)
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
+  __syncthreads();
+  if (tid == 0) {
+    if (MODE == MODE_STEP) {
+      fb_store_issue(sm, ring_at(p, (h + 1) & 3, block0));
+    } else {
+      for (uint32_t sl = 0; sl < 4; ++sl) fb_store_issue(sm, ring_at(p, sl, block0));
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  if (obs64) {
+    for (int e = 0; e < ne; e += 2)
+      if (e + (int)hh < ne) {
+        const uint32_t el = (uint32_t)(warp * 32 + e) + hh, ra = l2 ^ (el & 15u);
+        const uint4 q = *reinterpret_cast<const uint4 *>(&sm.fb[el * 32u + l2]);
+        uint64_t *ob = obs64 + (wbase + e + hh) * 128;
+        put_rows(ob, 3u, ra, q);
+        if (MODE != MODE_STEP || ((reset_mask >> (e + hh)) & 1u)) {
+          put_rows(ob, 0u, ra, q);
+          put_rows(ob, 1u, ra, q);
+          put_rows(ob, 2u, ra, q);
         }
-      } else {
-        rg[lane] = v; rg[32 + lane] = v; rg[64 + lane] = v; rg[96 + lane] = v;
-        if (ob) { ob[lane] = v; ob[32 + lane] = v; ob[64 + lane] = v; ob[96 + lane] = v; }
       }
+  }
+  if (MODE == MODE_STEP) {  // reset envs: the other three ring slots hold the reset display too
+    uint32_t rm = reset_mask;
+    while (rm) {
+      const int e = __ffs(rm) - 1;
+      rm &= rm - 1;
+      const uint64_t v = sm.fb[(uint32_t)(warp * 32 + e) * 32u + lane];  // position order = ring order
+      ring_at(p, s0, wbase + e)[lane] = v;
+      ring_at(p, s1, wbase + e)[lane] = v;
+      ring_at(p, s2, wbase + e)[lane] = v;
     }
   }
 
@@ -709,7 +741,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
         else atomicAdd(&p.s.stats[tid], acc);
       }
     }
-  }
+  }  if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem outlives the store
 }
 
 // ---------------------------------------------------------------- auxiliary kernels
@@ -791,12 +823,13 @@ __global__ void get_states_kernel(StepParams p, const uint64_t *__restrict__ ids
       for (int q = 0; q < 4; ++q) c[56 + 4 * k + q] = (uint8_t)(f[k] >> (8 * q));
   }
   // display (slot h) and history planes 0..2 = slots h-3, h-2, h-1
-  const uint8_t *rg = reinterpret_cast<const uint8_t *>(p.s.ring + env * 128);
+  // canonical byte i = row i>>3, byte i&7; the ring holds row r at position r ^ (env & 15)
   for (int i = t; i < 256; i += blockDim.x) {
-    c[80 + i] = rg[(h & 3) * 256 + i];
-    c[336 + i] = rg[((h + 1) & 3) * 256 + i];
-    c[592 + i] = rg[((h + 2) & 3) * 256 + i];
-    c[848 + i] = rg[((h + 3) & 3) * 256 + i];
+    const uint32_t j = (((uint32_t)i >> 3) ^ (uint32_t)(env & 15u)) * 8u + ((uint32_t)i & 7u);
+    c[80 + i] = reinterpret_cast<const uint8_t *>(ring_at(p, h & 3, env))[j];
+    c[336 + i] = reinterpret_cast<const uint8_t *>(ring_at(p, (h + 1) & 3, env))[j];
+    c[592 + i] = reinterpret_cast<const uint8_t *>(ring_at(p, (h + 2) & 3, env))[j];
+    c[848 + i] = reinterpret_cast<const uint8_t *>(ring_at(p, (h + 3) & 3, env))[j];
   }
   const uint64_t dirty = p.s.dirty[env];
   const uint8_t *ram = p.s.ram + env * 4096ull;
@@ -820,12 +853,12 @@ __global__ void set_state_kernel(StepParams p, uint64_t env, const uint8_t *__re
     p.s.stack[env * 2 + 1] = make_uint4(u32(40), u32(44), u32(48), u32(52));
     p.s.dirty[env] = ~0ull;  // whole RAM materialised from the canonical bytes
   }
-  uint8_t *rg = reinterpret_cast<uint8_t *>(p.s.ring + env * 128);
   for (int i = t; i < 256; i += blockDim.x) {
-    rg[(h & 3) * 256 + i] = c[80 + i];
-    rg[((h + 1) & 3) * 256 + i] = c[336 + i];
-    rg[((h + 2) & 3) * 256 + i] = c[592 + i];
-    rg[((h + 3) & 3) * 256 + i] = c[848 + i];
+    const uint32_t j = (((uint32_t)i >> 3) ^ (uint32_t)(env & 15u)) * 8u + ((uint32_t)i & 7u);
+    reinterpret_cast<uint8_t *>(ring_at(p, h & 3, env))[j] = c[80 + i];
+    reinterpret_cast<uint8_t *>(ring_at(p, (h + 1) & 3, env))[j] = c[336 + i];
+    reinterpret_cast<uint8_t *>(ring_at(p, (h + 2) & 3, env))[j] = c[592 + i];
+    reinterpret_cast<uint8_t *>(ring_at(p, (h + 3) & 3, env))[j] = c[848 + i];
   }
   uint8_t *ram = p.s.ram + env * 4096ull;
   for (int i = t; i < 4096; i += blockDim.x) ram[i] = c[1104 + i];
