@@ -304,7 +304,6 @@ octax_status compile_expr(const char *src, const char *what, Program &prog) {
 // folded in.
 void build_desc_table(uint32_t quirks, uint32_t out[kDescEntries]) {
   for (uint32_t k = 0; k < kDescEntries; ++k) out[k] = 0;
-  const uint32_t shift_reads = (quirks & OCTAX_Q_SHIFT_VY) ? D_RY : D_RX;
   for (uint32_t hi = 0; hi < 14; ++hi)
     for (uint32_t n = 0; n < 16; ++n) {
       uint32_t d = 0;
@@ -312,30 +311,29 @@ void build_desc_table(uint32_t quirks, uint32_t out[kDescEntries]) {
         case 0x0: d = D_OK; break;  // 00E0 / 00EE / 0NNN decided from the full word
         case 0x1: d = D_OK | D_PCJ; break;
         case 0x2: d = D_OK | D_PCJ | D_CALL; break;
-        case 0x3: d = D_OK | D_SKIPEQ | D_RX; break;
-        case 0x4: d = D_OK | D_SKIPNE | D_RX; break;
-        case 0x5: d = n == 0 ? (D_OK | D_SKIPEQ | D_BVY | D_RX | D_RY) : 0u; break;
+        case 0x3: d = D_OK | D_SKIPEQ; break;
+        case 0x4: d = D_OK | D_SKIPNE; break;
+        case 0x5: d = n == 0 ? (D_OK | D_SKIPEQ | D_BVY) : 0u; break;
         case 0x6: d = D_OK | D_WVX; break;
-        case 0x7: d = D_OK | D_WVX | D_VSADD | D_RX; break;
+        case 0x7: d = D_OK | D_WVX | D_VSADD; break;
         case 0x8:
           if (n <= 7 || n == 0xE) {
             d = D_OK | D_WVX | D_VSALU;
             if (n >= 4 || ((quirks & OCTAX_Q_VF_RESET) && n >= 1)) d |= D_WVF;
-            d |= n == 0 ? D_RY : (n == 6 || n == 0xE) ? shift_reads : (D_RX | D_RY);
           }
           break;
-        case 0x9: d = n == 0 ? (D_OK | D_SKIPNE | D_BVY | D_RX | D_RY) : 0u; break;
+        case 0x9: d = n == 0 ? (D_OK | D_SKIPNE | D_BVY) : 0u; break;
         case 0xA: d = D_OK | D_INNN; break;
-        case 0xB: d = D_OK | D_BJMP | ((quirks & OCTAX_Q_JUMP_VX) ? D_RX : 0u); break;
+        case 0xB: d = D_OK | D_BJMP; break;
         case 0xC: d = D_OK | D_RND; break;
-        case 0xD: d = D_OK | D_DRAW | D_RX | D_RY; break;
+        case 0xD: d = D_OK | D_DRAW; break;
       }
       out[(hi << 4) | n] = d;
     }
   struct { uint32_t op; uint32_t d; } ef[] = {
-      {0xE09E, D_SKIPKEY | D_RX}, {0xE0A1, D_SKIPNKEY | D_RX}, {0xF007, D_WVX | D_VSDT}, {0xF00A, D_WAIT},
-      {0xF015, D_DTW | D_RX},     {0xF018, D_STW | D_RX},      {0xF01E, D_IADD | D_RX},  {0xF029, D_IFONT | D_RX},
-      {0xF033, D_MEM | D_RX},     {0xF055, D_MEM | D_RX},      {0xF065, D_MEM}};
+      {0xE09E, D_SKIPKEY}, {0xE0A1, D_SKIPNKEY}, {0xF007, D_WVX | D_VSDT}, {0xF00A, D_WAIT},
+      {0xF015, D_DTW},     {0xF018, D_STW},      {0xF01E, D_IADD},         {0xF029, D_IFONT},
+      {0xF033, D_MEM},     {0xF055, D_MEM},      {0xF065, D_MEM}};
   for (auto &e : ef) out[desc_index(e.op)] = D_OK | D_YCHK | e.d | (((e.op >> 4) & 15u) << 28);
 }
 
@@ -457,7 +455,7 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   const uint64_t n = n_envs;
   size_t off = 0;
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
-  size_t o_img = carve(kStageBytes), o_stats = carve(64), o_regs = carve(16 * n), o_ctrl = carve(16 * n),
+  size_t o_img = carve(kStageBytes), o_dec = carve(8 * kDecEntries), o_stats = carve(64), o_regs = carve(16 * n), o_ctrl = carve(16 * n),
          o_book = carve(16 * n), o_stack = carve(32 * n), o_dirty = carve(8 * n),
          o_ring = carve(1024 * ((n + kBlock - 1) / kBlock * kBlock)),
          o_ram = carve(4096 * n);
@@ -466,6 +464,7 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   if (ce != cudaSuccess) { free_env(e); return cuda_err(ce, "cudaMalloc(state)"); }
   uint8_t *base = (uint8_t *)e->block;
   p.s.image = base + o_img;
+  p.s.dec = (const uint2 *)(base + o_dec);
   p.s.stats = (unsigned long long *)(base + o_stats);
   p.s.regs = (uint4 *)(base + o_regs);
   p.s.ctrl = (uint4 *)(base + o_ctrl);
@@ -482,8 +481,19 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   memset(image, 0, sizeof image);
   memcpy(image + 0x50, kFont, sizeof kFont);
   memcpy(image + 0x200, rom, rom_len);
-  build_desc_table(spec->quirks, reinterpret_cast<uint32_t *>(image + kImageBytes));
+  const uint32_t *dtab = reinterpret_cast<const uint32_t *>(image + kImageBytes);
+  build_desc_table(spec->quirks, const_cast<uint32_t *>(dtab));
+  std::vector<uint2> dec(kDecEntries);
+  for (uint32_t pc = 0; pc < kDecEntries; ++pc) {
+    if (pc <= 0xFFEu) {
+      make_entry(((uint32_t)image[pc] << 8) | image[pc + 1], dtab, spec->quirks, dec[pc].x, dec[pc].y);
+    } else {
+      dec[pc] = make_uint2(E_BAD, 0u);  // fetch past 0xFFE halts (A17)
+    }
+  }
   ce = cudaMemcpyAsync(base + o_img, image, kStageBytes, cudaMemcpyHostToDevice, e->stream);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpyAsync(base + o_dec, dec.data(), 8 * kDecEntries, cudaMemcpyHostToDevice, e->stream);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->stream);
   if (ce != cudaSuccess) { free_env(e); return cuda_err(ce, "upload image"); }
   if (e->obs_format != OCTAX_OBS_PACKED) {

@@ -19,15 +19,15 @@ constexpr uint32_t kStageBytes = kImageBytes + 4 * kDescEntries;  // image + dec
 // descriptor bits instead of re-deriving the class from the opcode every cycle.
 // E/F entries carry the expected y nibble (bits 28..31, checked under D_YCHK): with
 // the injective nibble hash below, (hi, hash, y) determines the whole word.
-// D_RX / D_RY: the instruction reads V[x] / V[y] (deferred-DXYN resolution trigger
-// when that register is VF and a queued draw's VF result is still pending).
 enum : uint32_t {
   D_OK = 1u << 0, D_YCHK = 1u << 1, D_SKIPEQ = 1u << 2, D_SKIPNE = 1u << 3, D_BVY = 1u << 4,
   D_SKIPKEY = 1u << 5, D_SKIPNKEY = 1u << 6, D_WVX = 1u << 7, D_WVF = 1u << 8, D_VSADD = 1u << 9,
   D_VSALU = 1u << 10, D_VSDT = 1u << 11, D_WAIT = 1u << 12, D_PCJ = 1u << 13, D_CALL = 1u << 14,
   D_BJMP = 1u << 15, D_INNN = 1u << 16, D_IADD = 1u << 17, D_IFONT = 1u << 18, D_DTW = 1u << 19,
   D_STW = 1u << 20, D_RND = 1u << 21, D_MEM = 1u << 22, D_DRAW = 1u << 23,
-  D_RX = 1u << 24, D_RY = 1u << 25
+  // predecoded-entry only (never in the descriptor table)
+  E_BAD = 1u << 25, E_RET = 1u << 26, E_CLS = 1u << 27,
+  D_EXEC = 0x00FFFFFCu  // descriptor bits that carry over into an entry
 };
 
 // hi << 4 | low nibble; for EXnn / FXnn the nibble is (n - 2y) & 15, which is
@@ -38,6 +38,29 @@ __host__ __device__
 inline uint32_t desc_index(uint32_t op) {
   const uint32_t hi = op >> 12, y = (op >> 4) & 15u, n = op & 15u;
   return (hi << 4) | (hi >= 14u ? ((n + 14u * y) & 15u) : n);
+}
+
+// Predecoded instruction: what the core needs from the 16-bit word at a PC, with every
+// decision that depends on the word alone taken once (per handle, on the host, for all
+// 4096 PCs of the pristine image; on the device only for a PC in a dirty RAM block).
+//   .x = execution flags (D_* bits of D_EXEC, E_BAD / E_RET / E_CLS) | x << 28
+//   .y = kx | ky << 11 | nn << 24, with k* = 132 * register index (the smem V offset
+//        before the per-lane XOR, see VREG) -- kx addresses the register the word
+//        reads as "VX": V[x], or V0 for BNNN without the JUMP_VX quirk.
+constexpr uint32_t kDecEntries = 4097;  // PCs 0..0xFFF, entry 0x1000 (PC past memory) halts
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline void make_entry(uint32_t op, const uint32_t *dtab, uint32_t quirks, uint32_t &ex, uint32_t &ey) {
+  const uint32_t x = (op >> 8) & 15u, y = (op >> 4) & 15u, nn = op & 255u;
+  const uint32_t d = dtab[desc_index(op)];
+  const bool bad = (d & D_OK) == 0u || ((d & D_YCHK) != 0u && y != (d >> 28));
+  uint32_t f = bad ? E_BAD : (d & D_EXEC);
+  if (op == 0x00EEu) f |= E_RET;
+  if (op == 0x00E0u) f |= E_CLS;
+  const uint32_t rx = ((d & D_BJMP) != 0u && (quirks & 4u) == 0u) ? 0u : x;  // 4 = OCTAX_Q_JUMP_VX
+  ex = f | (x << 28);
+  ey = (132u * rx) | ((132u * y) << 11) | (nn << 24);
 }
 
 // expression bytecode (postfix, evaluated with top-of-stack in a register)
@@ -76,6 +99,7 @@ struct DevState {
   uint64_t ring_stride;  // u64 per ring slot = n_pad * 32
   unsigned long long *stats;  // [4] {returns, episodes, steps, err}
   const uint8_t *image;       // [4096] pristine image: zeros, font at 0x50, ROM at 0x200
+  const uint2 *dec;           // [kDecEntries] predecoded instruction at every PC (make_entry)
 };
 
 struct StepParams {

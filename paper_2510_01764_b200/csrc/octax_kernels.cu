@@ -148,6 +148,7 @@ struct Lane {
   uint64_t dirty;   // copy-on-write mask: block b (64 B) of RAM lives in HBM
   uint8_t *ram;
   uint32_t stk_dirty;
+  uint2 dec;        // predecoded word at pc, loaded one cycle ahead (latency hidden)
 };
 
 #define VREG(k) sm.V[((k) << 7) + ((uint32_t)tid ^ ((uint32_t)(k) << 2))]
@@ -169,7 +170,7 @@ __device__ __forceinline__ void wr(const Smem &sm, Lane &L, uint32_t a, uint32_t
   L.ram[a] = (uint8_t)v;
 }
 
-__device__ __forceinline__ void power_on(Smem &sm, Lane &L, int tid) {
+__device__ __forceinline__ void power_on(Smem &sm, Lane &L, const StepParams &p, int tid) {
 #pragma unroll
   for (int k = 0; k < 16; ++k) VREG(k) = 0;
 #pragma unroll
@@ -178,6 +179,7 @@ __device__ __forceinline__ void power_on(Smem &sm, Lane &L, int tid) {
   for (int r = 0; r < 32; ++r) sm.fb[tid * 32 + r] = 0;
   L.pc = 0x200; L.I = 0; L.sp = 0; L.dt = 0; L.st = 0; L.halted = 0; L.keys = 0; L.draw = 0;
   L.dirty = 0;
+  L.dec = __ldg(p.s.dec + 0x200);
   L.stk_dirty = 1;
 }
 
@@ -289,40 +291,86 @@ __device__ __forceinline__ void draw_lanes(Smem &sm, Lane &L, const StepParams &
   if (vfw) VREG(15) = (uint8_t)(hit != 0ull);
 }
 
+// DXYN, grouped: the warp's drawing lanes are served 32/G at a time with G = 8 or 16
+// >= the warp's largest row count; lane r of group g XORs row r of the g-th pending
+// drawer (rank order), so a pass costs one row step for up to 4 drawers.  Cheaper than
+// the lane-parallel loop (maxr row steps) when few lanes of the warp draw -- the common
+// case.  dm = lanes with >= 1 row to draw; DXY0 lanes get VF = 0.
+__device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepParams &p, int tid, int lane,
+                                            uint64_t block0, uint32_t dm, uint32_t x0, uint32_t y0, uint32_t base,
+                                            uint32_t nrows, uint32_t maxr, bool wdirty, uint32_t quirks, bool vfw) {
+  const bool wrap = (quirks & 8u) != 0;
+  const uint32_t lg = maxr <= 8u ? 3u : 4u, P = 32u >> lg;
+  const uint32_t grp = (uint32_t)lane >> lg, r = (uint32_t)lane & ((1u << lg) - 1u);
+  const uint32_t gmask = lg == 3u ? 0xFFu : 0xFFFFu;
+  const uint32_t prm = x0 | (y0 << 6) | (base << 11) | (nrows << 23);
+  const uint32_t wl = (uint32_t)tid & ~31u;
+  const bool mine = ((dm >> lane) & 1u) != 0u;
+  const uint32_t rank = (uint32_t)__popc(dm & ((1u << lane) - 1u));
+  bool myhit = false;
+  for (uint32_t first = 0; dm; first += P) {
+    uint32_t b = dm;  // my group's drawer = the grp-th pending one
+    b = grp >= 1u ? b & (b - 1u) : b;
+    b = grp >= 2u ? b & (b - 1u) : b;
+    b = grp >= 3u ? b & (b - 1u) : b;
+    const uint32_t own = b ? (uint32_t)(__ffs(b) - 1) : 0u;
+    const uint32_t q = __shfl_sync(kFull, prm, own);
+    uint64_t od = 0;
+    if (wdirty) od = __shfl_sync(kFull, L.dirty, own);
+    bool hit = false;
+    if (b != 0u && r < (q >> 23)) {
+      const uint32_t ox = q & 63u, oe = wl + own, a = ((q >> 11) & 0xFFFu) + r;
+      uint32_t byte = 0;
+      if (a <= 0xFFFu)
+        byte = ((od >> (a >> 6)) & 1ull) ? (uint32_t)p.s.ram[(block0 + oe) * 4096ull + a] : (uint32_t)sm.img[a];
+      const uint32_t yy = (((q >> 6) & 31u) + r) & 31u, q8 = (ox >> 3) * 8u;
+      const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> (ox & 7u), 0, 0x4401);
+      const uint64_t mk = wrap ? ((w << q8) | (q8 ? (w >> (64u - q8)) : 0ull)) : (w << q8);
+      uint64_t *row = &sm.fb[oe * 32u + (yy ^ (oe & 15u))];
+      const uint64_t old = *row;
+      *row = old ^ mk;
+      hit = (old & mk) != 0ull;
+    }
+    const uint32_t hb = __ballot_sync(kFull, hit);
+    const uint32_t g = rank - first;
+    if (mine & (g < P)) myhit = ((hb >> (g << lg)) & gmask) != 0u;
+    dm &= dm - 1u;  // retire this pass's P drawers
+    dm &= dm - 1u;
+    if (P == 4u) { dm &= dm - 1u; dm &= dm - 1u; }
+  }
+  if (vfw) VREG(15) = (uint8_t)myhit;
+}
+
 template <bool Q0>
 __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, int tid, int lane, uint64_t block0,
                                       uint32_t gid, bool part, bool &wdirty) {
   const uint32_t quirks = Q0 ? 0u : p.quirks;  // Q0: modern profile specialisation
   bool act = part & (L.halted == 0u);
   const uint32_t pc = L.pc;
-  const bool oob = pc > 0xFFEu;
-  // ---- fetch: one aligned 16-bit load from the smem image (slow path: odd PC or dirty block)
-  const uint32_t w16 = *reinterpret_cast<const uint16_t *>(sm.img + (pc & 0xFFEu));
-  uint32_t op = __byte_perm(w16, 0, 0x4401);
-  bool slow = act & !oob & ((pc & 1u) != 0u);
-  if (wdirty) slow |= act & !oob & (((L.dirty >> (pc >> 6)) & 1ull) != 0ull);
-  if (__any_sync(kFull, slow)) {
-    if (slow) op = (rd(sm, L, pc) << 8) | rd(sm, L, pc + 1);
+  // ---- fetch + decode: the predecoded word at PC (L1-resident table, loaded at the end
+  //      of the previous cycle; PCs past 0xFFE halt through the table).  Slow path: PC in
+  //      a dirty RAM block (self-modifying code).
+  uint2 e = L.dec;
+  if (wdirty) {
+    const bool slow = act & (pc <= 0xFFEu) & (((L.dirty >> (pc >> 6)) & 3ull) != 0ull);
+    if (__any_sync(kFull, slow)) {
+      if (slow) make_entry((rd(sm, L, pc) << 8) | rd(sm, L, pc + 1), sm.dtab, quirks, e.x, e.y);
+    }
   }
-  // ---- decode: one descriptor load replaces the per-class opcode compares
-  const uint32_t x = (op >> 8) & 15u, y = (op >> 4) & 15u, n = op & 15u, nn = op & 255u,
-                 nnn = op & 0xFFFu;
-  const uint32_t d = sm.dtab[desc_index(op)];
-  const bool is_ret = op == 0x00EEu, is_cls = op == 0x00E0u;
+  const uint32_t d = e.x, x = d >> 28, nn = e.y >> 24, n = nn & 15u, nnn = (x << 8) | nn;
+  const bool is_ret = (d & E_RET) != 0u, is_cls = (d & E_CLS) != 0u;
   // ---- faults halt the lane (A17, A20)
-  bool bad = oob | ((d & D_OK) == 0u) | (((d & D_YCHK) != 0u) & (y != (d >> 28)));
+  bool bad = (d & E_BAD) != 0u;
   bad |= is_ret & (L.sp == 0u);
   bad |= ((d & D_CALL) != 0u) & (L.sp == 16u);
   L.halted |= (uint32_t)(act & bad);
   act = act & !bad;
-  // ---- deferred DXYN: resolve the queues before anything that observes their effect:
-  //      a read of VF while a queued draw still owns it, CLS, a RAM write (sprite bytes),
-  //      or a draw into a full queue
-  const uint32_t vx = VREG(x), vy = VREG(y);
+  // V[k] of this lane lives at k * 132 ^ tid (VREG); kx = V[x], or V0 for BNNN
+  const uint32_t vx = sm.V[(e.y & 0x7FFu) ^ (uint32_t)tid], vy = sm.V[((e.y >> 11) & 0x7FFu) ^ (uint32_t)tid];
   // ---- stack
   OCTAX_CHECK(!(act & is_ret) || (L.sp >= 1u && L.sp <= 16u));
   OCTAX_CHECK(!(act & ((d & D_CALL) != 0u)) || L.sp < 16u);
-  OCTAX_CHECK(x < 16u && y < 16u && tid < kBlock);
+  OCTAX_CHECK(x < 16u && tid < kBlock);
   uint32_t ret_pc = 0;
   if (act & is_ret) ret_pc = sm.stk[(L.sp - 1u) * kBlock + tid];
   if (act & ((d & D_CALL) != 0u)) { sm.stk[L.sp * kBlock + tid] = (uint16_t)(pc + 2u); L.stk_dirty = 1; }
@@ -364,13 +412,14 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   npc = (d & D_PCJ) ? nnn : npc;  // 1NNN, 2NNN
   npc = is_ret ? ret_pc : npc;
   npc = (((d & D_WAIT) != 0u) & (L.keys == 0u)) ? pc : npc;  // A16: FX0A re-executes while no key
-  if (act & ((d & D_BJMP) != 0u)) npc = (nnn + VREG((quirks & 4u) ? x : 0u)) & 0xFFFu;
+  npc = (d & D_BJMP) ? ((nnn + vx) & 0xFFFu) : npc;  // vx = V0 or V[x] (JUMP_VX quirk)
   uint32_t I2 = L.I;
   I2 = (d & D_INNN) ? nnn : I2;
   I2 = (d & D_IADD) ? ((I2 + vx) & 0xFFFFu) : I2;
   I2 = (d & D_IFONT) ? (0x50u + 5u * (vx & 15u)) : I2;
   if (act) {
     L.pc = npc & 0xFFFFu;
+    L.dec = __ldg(p.s.dec + min(L.pc, 0x1000u));  // next cycle's word, in flight meanwhile
     L.I = I2;
     L.sp = L.sp + (uint32_t)((d & D_CALL) != 0u) - (uint32_t)is_ret;
     L.dt = (d & D_DTW) ? vx : L.dt;
@@ -418,7 +467,12 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     const uint32_t y0 = vy & 31u;
     const uint32_t nrows = do_draw ? (((quirks & 8u) != 0u) ? n : min(n, 32u - y0)) : 0u;
     const uint32_t maxr = __reduce_max_sync(kFull, nrows);
-    if (maxr <= kLaneDrawMax)
+    const uint32_t dm = __ballot_sync(kFull, nrows != 0u);
+    // passes of the grouped draw vs row steps of the lane-parallel one (uniform choice)
+    const uint32_t passes = ((uint32_t)__popc(dm) + (maxr <= 8u ? 3u : 1u)) >> (maxr <= 8u ? 2 : 1);
+    if (4u * passes <= maxr + 1u)
+      draw_groups(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
+    else if (maxr <= kLaneDrawMax)
       draw_lanes(sm, L, p, tid, do_draw, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
     else
       draw_coop(sm, L, p, tid, lane, block0, do_draw, vx & 63u, y0, L.I & 0xFFFu, n, do_draw, quirks);
@@ -539,6 +593,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     L.dirty = p.s.dirty[env];
     L.ram = p.s.ram + env * 4096ull;
   }
+  L.dec = __ldg(p.s.dec + min(L.pc, 0x1000u));
   __syncthreads();  // mbarrier initialised
   stage_wait(sm);
   bool wdirty = __any_sync(kFull, L.dirty != 0ull);  // any lane with private RAM blocks
@@ -647,7 +702,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   // ---- same-step auto-reset: power-on + startup segments (warp-uniform)
   const uint32_t reset_mask = __ballot_sync(kFull, resetting);
   if (reset_mask) {
-    if (resetting) power_on(sm, L, tid);
+    if (resetting) power_on(sm, L, p, tid);
     __syncwarp();
     for (uint32_t seg = 0; seg < p.n_startup; ++seg) {
       if (resetting) L.keys = p.startup_keys[seg];
