@@ -48,5 +48,18 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
     return so
 
 
+def build_variant(out: str, defines=()) -> str:
+    """Build the library from the current sources into `out` (A/B experiments)."""
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-o", out, *SOURCES]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed")
+    return out
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))
+    if "--out" in sys.argv:
+        print(build_variant(sys.argv[sys.argv.index("--out") + 1]))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

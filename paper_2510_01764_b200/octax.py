@@ -14,6 +14,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # OCTAX_CHECKED=1 selects the bounds-checked build (device asserts; tests / debugging)
 SO_PATH = os.path.join(_HERE, "liboctax_checked.so" if os.environ.get("OCTAX_CHECKED") == "1" else "liboctax.so")
+# OCTAX_LIB=<path>: load another build of the same ABI (A/B timing of kernel variants)
+SO_PATH = os.environ.get("OCTAX_LIB", SO_PATH)
 
 CANON_BYTES = 5200
 OBS_PACKED = 0
