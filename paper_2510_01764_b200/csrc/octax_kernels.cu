@@ -152,6 +152,10 @@ struct Lane {
 };
 
 #define VREG(k) sm.V[((k) << 7) + ((uint32_t)tid ^ ((uint32_t)(k) << 2))]
+// Flag test written with a two-bit mask (kPad is never set in an entry): keeps the
+// compiler from lowering a single-bit test to shift + and + compare (one LOP3 instead).
+constexpr uint32_t kPad = 1u << 24;
+#define HAS(d, F) (((d) & ((F) | kPad)) != 0u)
 
 __device__ __forceinline__ uint32_t rd(const Smem &sm, const Lane &L, uint32_t a) {
   OCTAX_CHECK(a < 4096u);
@@ -291,54 +295,41 @@ __device__ __forceinline__ void draw_lanes(Smem &sm, Lane &L, const StepParams &
   if (vfw) VREG(15) = (uint8_t)(hit != 0ull);
 }
 
-// DXYN, grouped: the warp's drawing lanes are served 32/G at a time with G = 8 or 16
-// >= the warp's largest row count; lane r of group g XORs row r of the g-th pending
-// drawer (rank order), so a pass costs one row step for up to 4 drawers.  Cheaper than
-// the lane-parallel loop (maxr row steps) when few lanes of the warp draw -- the common
-// case.  dm = lanes with >= 1 row to draw; DXY0 lanes get VF = 0.
+// DXYN, grouped, one pass: the k drawing lanes of the warp (k <= 32 / G, G = 2^lg >= the
+// warp's largest row count) publish packed parameters to a per-warp smem slot by rank;
+// lane r of group g XORs row r of drawer g, so all drawers cost one row step.  The
+// collision bits come back with one ballot.  dm = lanes with >= 1 row; DXY0 -> VF = 0.
 __device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepParams &p, int tid, int lane,
                                             uint64_t block0, uint32_t dm, uint32_t x0, uint32_t y0, uint32_t base,
-                                            uint32_t nrows, uint32_t maxr, bool wdirty, uint32_t quirks, bool vfw) {
+                                            uint32_t nrows, uint32_t lg, bool wdirty, uint32_t quirks, bool vfw) {
   const bool wrap = (quirks & 8u) != 0;
-  const uint32_t lg = maxr <= 8u ? 3u : 4u, P = 32u >> lg;
-  const uint32_t grp = (uint32_t)lane >> lg, r = (uint32_t)lane & ((1u << lg) - 1u);
-  const uint32_t gmask = lg == 3u ? 0xFFu : 0xFFFFu;
-  const uint32_t prm = x0 | (y0 << 6) | (base << 11) | (nrows << 23);
-  const uint32_t wl = (uint32_t)tid & ~31u;
+  const uint32_t warp = (uint32_t)tid >> 5, wl = (uint32_t)tid & ~31u;
   const bool mine = ((dm >> lane) & 1u) != 0u;
   const uint32_t rank = (uint32_t)__popc(dm & ((1u << lane) - 1u));
-  bool myhit = false;
-  for (uint32_t first = 0; dm; first += P) {
-    uint32_t b = dm;  // my group's drawer = the grp-th pending one
-    b = grp >= 1u ? b & (b - 1u) : b;
-    b = grp >= 2u ? b & (b - 1u) : b;
-    b = grp >= 3u ? b & (b - 1u) : b;
-    const uint32_t own = b ? (uint32_t)(__ffs(b) - 1) : 0u;
-    const uint32_t q = __shfl_sync(kFull, prm, own);
-    uint64_t od = 0;
-    if (wdirty) od = __shfl_sync(kFull, L.dirty, own);
-    bool hit = false;
-    if (b != 0u && r < (q >> 23)) {
-      const uint32_t ox = q & 63u, oe = wl + own, a = ((q >> 11) & 0xFFFu) + r;
-      uint32_t byte = 0;
-      if (a <= 0xFFFu)
-        byte = ((od >> (a >> 6)) & 1ull) ? (uint32_t)p.s.ram[(block0 + oe) * 4096ull + a] : (uint32_t)sm.img[a];
-      const uint32_t yy = (((q >> 6) & 31u) + r) & 31u, q8 = (ox >> 3) * 8u;
-      const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> (ox & 7u), 0, 0x4401);
-      const uint64_t mk = wrap ? ((w << q8) | (q8 ? (w >> (64u - q8)) : 0ull)) : (w << q8);
-      uint64_t *row = &sm.fb[oe * 32u + (yy ^ (oe & 15u))];
-      const uint64_t old = *row;
-      *row = old ^ mk;
-      hit = (old & mk) != 0ull;
-    }
-    const uint32_t hb = __ballot_sync(kFull, hit);
-    const uint32_t g = rank - first;
-    if (mine & (g < P)) myhit = ((hb >> (g << lg)) & gmask) != 0u;
-    dm &= dm - 1u;  // retire this pass's P drawers
-    dm &= dm - 1u;
-    if (P == 4u) { dm &= dm - 1u; dm &= dm - 1u; }
+  if (mine) sm.dprm[warp][rank] = x0 | (y0 << 6) | (base << 11) | (nrows << 23) | ((uint32_t)lane << 27);
+  __syncwarp();
+  const uint32_t g = (uint32_t)lane >> lg, r = (uint32_t)lane & ((1u << lg) - 1u);
+  const bool gv = g < (uint32_t)__popc(dm);
+  const uint32_t q = gv ? sm.dprm[warp][g] : 0u;
+  const uint32_t own = q >> 27, oe = wl + own;
+  uint64_t od = 0;
+  if (wdirty) od = __shfl_sync(kFull, L.dirty, own);
+  bool hit = false;
+  if (gv && r < ((q >> 23) & 15u)) {
+    const uint32_t ox = q & 63u, a = ((q >> 11) & 0xFFFu) + r;
+    uint32_t byte = 0;
+    if (a <= 0xFFFu)
+      byte = ((od >> (a >> 6)) & 1ull) ? (uint32_t)p.s.ram[(block0 + oe) * 4096ull + a] : (uint32_t)sm.img[a];
+    const uint32_t yy = (((q >> 6) & 31u) + r) & 31u, q8 = ox & 0x38u;
+    const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> (ox & 7u), 0, 0x4401);
+    const uint64_t mk = wrap ? ((w << q8) | (q8 ? (w >> (64u - q8)) : 0ull)) : (w << q8);
+    uint64_t *row = &sm.fb[oe * 32u + (yy ^ (oe & 15u))];
+    const uint64_t old = *row;
+    *row = old ^ mk;
+    hit = (old & mk) != 0ull;
   }
-  if (vfw) VREG(15) = (uint8_t)myhit;
+  const uint32_t hb = __ballot_sync(kFull, hit);
+  if (vfw) VREG(15) = (uint8_t)(mine && ((hb >> (rank << lg)) & ((1u << (1u << lg)) - 1u)) != 0u);
 }
 
 template <bool Q0>
@@ -358,27 +349,25 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     }
   }
   const uint32_t d = e.x, x = d >> 28, nn = e.y >> 24, n = nn & 15u, nnn = (x << 8) | nn;
-  const bool is_ret = (d & E_RET) != 0u, is_cls = (d & E_CLS) != 0u;
+  const bool is_ret = HAS(d, E_RET), is_cls = HAS(d, E_CLS), call = HAS(d, D_CALL);
   // ---- faults halt the lane (A17, A20)
-  bool bad = (d & E_BAD) != 0u;
-  bad |= is_ret & (L.sp == 0u);
-  bad |= ((d & D_CALL) != 0u) & (L.sp == 16u);
-  L.halted |= (uint32_t)(act & bad);
-  act = act & !bad;
+  const bool bad = HAS(d, E_BAD) || (is_ret && L.sp == 0u) || (call && L.sp == 16u);
+  L.halted |= (uint32_t)(act && bad);
+  act = act && !bad;
   // V[k] of this lane lives at k * 132 ^ tid (VREG); kx = V[x], or V0 for BNNN
-  const uint32_t vx = sm.V[(e.y & 0x7FFu) ^ (uint32_t)tid], vy = sm.V[((e.y >> 11) & 0x7FFu) ^ (uint32_t)tid];
+  const uint32_t ax = (e.y & 0x7FFu) ^ (uint32_t)tid, vx = sm.V[ax], vy = sm.V[((e.y >> 11) & 0x7FFu) ^ (uint32_t)tid];
   // ---- stack
-  OCTAX_CHECK(!(act & is_ret) || (L.sp >= 1u && L.sp <= 16u));
-  OCTAX_CHECK(!(act & ((d & D_CALL) != 0u)) || L.sp < 16u);
+  OCTAX_CHECK(!(act && is_ret) || (L.sp >= 1u && L.sp <= 16u));
+  OCTAX_CHECK(!(act && call) || L.sp < 16u);
   OCTAX_CHECK(x < 16u && tid < kBlock);
   uint32_t ret_pc = 0;
-  if (act & is_ret) ret_pc = sm.stk[(L.sp - 1u) * kBlock + tid];
-  if (act & ((d & D_CALL) != 0u)) { sm.stk[L.sp * kBlock + tid] = (uint16_t)(pc + 2u); L.stk_dirty = 1; }
+  if (act && is_ret) ret_pc = sm.stk[(L.sp - 1u) * kBlock + tid];
+  if (act && call) { sm.stk[L.sp * kBlock + tid] = (uint16_t)(pc + 2u); L.stk_dirty = 1; }
   // ---- skips: 3XNN 5XY0 on equal, 4XNN 9XY0 on not-equal, EX9E / EXA1 on key
-  const bool eq = vx == ((d & D_BVY) ? vy : nn);
+  const bool eq = vx == (HAS(d, D_BVY) ? vy : nn);
   const bool keyd = ((L.keys >> (vx & 15u)) & 1u) != 0u;
-  const bool skip = (((d & D_SKIPEQ) != 0u) & eq) | (((d & D_SKIPNE) != 0u) & !eq) |
-                    (((d & D_SKIPKEY) != 0u) & keyd) | (((d & D_SKIPNKEY) != 0u) & !keyd);
+  const bool skip = (HAS(d, D_SKIPEQ) && eq) || (HAS(d, D_SKIPNE) && !eq) ||
+                    (HAS(d, D_SKIPKEY) && keyd) || (HAS(d, D_SKIPNKEY) && !keyd);
   // ---- ALU 8XYn; flag written after the result (A15); VF-reset quirk folded into D_WVF
   const uint32_t s = (quirks & 1u) ? vy : vx;
   const bool sub5 = n == 5u, sub7 = n == 7u;
@@ -386,12 +375,12 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   uint32_t sb = vy;
   sb = sub5 ? (vy ^ 255u) : sb;
   sb = sub7 ? (vx ^ 255u) : sb;
-  const uint32_t sum = sa + sb + (uint32_t)(sub5 | sub7);
+  const uint32_t sum = sa + sb + (uint32_t)(sub5 || sub7);
   uint32_t r8 = vy, f8 = 0u;
   r8 = (n == 1u) ? (vx | vy) : r8;
   r8 = (n == 2u) ? (vx & vy) : r8;
   r8 = (n == 3u) ? (vx ^ vy) : r8;
-  const bool add = (n == 4u) | sub5 | sub7;
+  const bool add = (n == 4u) || sub5 || sub7;
   r8 = add ? (sum & 255u) : r8;
   f8 = add ? (sum >> 8) : f8;
   r8 = (n == 6u) ? (s >> 1) : r8;
@@ -399,38 +388,38 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   r8 = (n == 0xEu) ? ((s << 1) & 255u) : r8;
   f8 = (n == 0xEu) ? (s >> 7) : f8;
   // ---- register writes
+  const bool wait = HAS(d, D_WAIT), nokey = L.keys == 0u;
   uint32_t nvx = nn;
-  nvx = (d & D_VSADD) ? ((vx + nn) & 255u) : nvx;
-  nvx = (d & D_VSALU) ? r8 : nvx;
-  nvx = (d & D_VSDT) ? L.dt : nvx;
-  nvx = (d & D_WAIT) ? (uint32_t)(__ffs(L.keys) - 1) : nvx;
-  const bool wvx = act & (((d & D_WVX) != 0u) | (((d & D_WAIT) != 0u) & (L.keys != 0u)));
-  if (wvx) VREG(x) = (uint8_t)nvx;
-  if (act & ((d & D_WVF) != 0u)) VREG(15) = (uint8_t)f8;
+  nvx = HAS(d, D_VSADD) ? ((vx + nn) & 255u) : nvx;
+  nvx = HAS(d, D_VSALU) ? r8 : nvx;
+  nvx = HAS(d, D_VSDT) ? L.dt : nvx;
+  nvx = wait ? (uint32_t)(__ffs(L.keys) - 1) : nvx;
+  if (act && (HAS(d, D_WVX) || (wait && !nokey))) sm.V[ax] = (uint8_t)nvx;
+  if (act && HAS(d, D_WVF)) VREG(15) = (uint8_t)f8;
   // ---- control flow and index / timer registers
   uint32_t npc = pc + (skip ? 4u : 2u);
-  npc = (d & D_PCJ) ? nnn : npc;  // 1NNN, 2NNN
+  npc = HAS(d, D_PCJ) ? nnn : npc;  // 1NNN, 2NNN
   npc = is_ret ? ret_pc : npc;
-  npc = (((d & D_WAIT) != 0u) & (L.keys == 0u)) ? pc : npc;  // A16: FX0A re-executes while no key
-  npc = (d & D_BJMP) ? ((nnn + vx) & 0xFFFu) : npc;  // vx = V0 or V[x] (JUMP_VX quirk)
+  npc = (wait && nokey) ? pc : npc;  // A16: FX0A re-executes while no key
+  npc = HAS(d, D_BJMP) ? ((nnn + vx) & 0xFFFu) : npc;  // vx = V0 or V[x] (JUMP_VX quirk)
   uint32_t I2 = L.I;
-  I2 = (d & D_INNN) ? nnn : I2;
-  I2 = (d & D_IADD) ? ((I2 + vx) & 0xFFFFu) : I2;
-  I2 = (d & D_IFONT) ? (0x50u + 5u * (vx & 15u)) : I2;
+  I2 = HAS(d, D_INNN) ? nnn : I2;
+  I2 = HAS(d, D_IADD) ? ((I2 + vx) & 0xFFFFu) : I2;
+  I2 = HAS(d, D_IFONT) ? (0x50u + 5u * (vx & 15u)) : I2;
   if (act) {
     L.pc = npc & 0xFFFFu;
     L.dec = __ldg(p.s.dec + min(L.pc, 0x1000u));  // next cycle's word, in flight meanwhile
     L.I = I2;
-    L.sp = L.sp + (uint32_t)((d & D_CALL) != 0u) - (uint32_t)is_ret;
-    L.dt = (d & D_DTW) ? vx : L.dt;
-    L.st = (d & D_STW) ? vx : L.st;
+    L.sp = L.sp + (uint32_t)call - (uint32_t)is_ret;
+    L.dt = HAS(d, D_DTW) ? vx : L.dt;
+    L.st = HAS(d, D_STW) ? vx : L.st;
   }
   const bool f33 = nn == 0x33u, f55 = nn == 0x55u;  // only meaningful under D_MEM
   // ---- vote-gated rare classes (one vote for CLS / CXNN / FX33-55-65 together)
-  const bool do_cls = act & is_cls;
-  const bool do_rnd = act & ((d & D_RND) != 0u);
-  const bool do_mem = act & ((d & D_MEM) != 0u);
-  if (__any_sync(kFull, do_cls | do_rnd | do_mem)) {
+  const bool do_cls = act && is_cls;
+  const bool do_rnd = act && HAS(d, D_RND);
+  const bool do_mem = act && HAS(d, D_MEM);
+  if (__any_sync(kFull, do_cls || do_rnd || do_mem)) {
   if (__any_sync(kFull, do_cls)) {
     if (do_cls) {
 #pragma unroll
@@ -462,16 +451,17 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     wdirty = __any_sync(kFull, L.dirty != 0ull);
   }
   }
-  const bool do_draw = act & ((d & D_DRAW) != 0u);
+  const bool do_draw = act && HAS(d, D_DRAW);
   if (__any_sync(kFull, do_draw)) {
     const uint32_t y0 = vy & 31u;
     const uint32_t nrows = do_draw ? (((quirks & 8u) != 0u) ? n : min(n, 32u - y0)) : 0u;
     const uint32_t maxr = __reduce_max_sync(kFull, nrows);
     const uint32_t dm = __ballot_sync(kFull, nrows != 0u);
-    // passes of the grouped draw vs row steps of the lane-parallel one (uniform choice)
-    const uint32_t passes = ((uint32_t)__popc(dm) + (maxr <= 8u ? 3u : 1u)) >> (maxr <= 8u ? 2 : 1);
-    if (4u * passes <= maxr + 1u)
-      draw_groups(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
+    // one grouped pass (groups of 2^lg >= maxr lanes) when the drawers fit and rows are
+    // many enough to beat maxr lane-parallel row steps (uniform choice)
+    const uint32_t lg = maxr > 1u ? 32u - (uint32_t)__clz(maxr - 1u) : 0u;
+    if (maxr >= 3u && (uint32_t)__popc(dm) <= (32u >> lg))
+      draw_groups(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, lg, wdirty, quirks, do_draw);
     else if (maxr <= kLaneDrawMax)
       draw_lanes(sm, L, p, tid, do_draw, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
     else
@@ -634,15 +624,19 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     const uint4 *rsrc = reinterpret_cast<const uint4 *>(ring_at(p, hh ? s1 : s0, wbase) + l2);
     uint64_t *odst = obs64 + wbase * 128 + hh * 32;
     int cur = sf ? ne : 0;
+    const uint4 *rp = rsrc + cur * 16;  // env `cur`'s chunk and obs row block, advanced per copy
+    uint64_t *opl = odst + cur * 128;
     for (uint32_t f = 0; f < p.frame_skip; ++f) {
       for (uint32_t k = 0; k < p.ipf; ++k) {
         const bool cp = cur < ne;
         uint4 q = make_uint4(0, 0, 0, 0);
-        if (cp) q = __ldcs(rsrc + cur * 16);
+        if (cp) q = __ldcs(rp);
         cycle<Q0>(sm, L, p, tid, lane, block0, gid, active, wdirty);
         if (cp) {
-          put_rows(odst + cur * 128, 0u, l2 ^ ((uint32_t)cur & 15u), q);
+          put_rows(opl, 0u, l2 ^ ((uint32_t)cur & 15u), q);
           ++cur;
+          rp += 16;
+          opl += 128;
         }
       }
       if (active && !L.halted) {
