@@ -311,9 +311,9 @@ void build_desc_table(uint32_t quirks, uint32_t out[kDescEntries]) {
         case 0x0: d = D_OK; break;  // 00E0 / 00EE / 0NNN decided from the full word
         case 0x1: d = D_OK | D_PCJ; break;
         case 0x2: d = D_OK | D_PCJ | D_CALL; break;
-        case 0x3: d = D_OK | D_SKIPEQ; break;
-        case 0x4: d = D_OK | D_SKIPNE; break;
-        case 0x5: d = n == 0 ? (D_OK | D_SKIPEQ | D_BVY) : 0u; break;
+        case 0x3: d = D_OK | D_SKIP; break;
+        case 0x4: d = D_OK | D_SKIP | D_SINV; break;
+        case 0x5: d = n == 0 ? (D_OK | D_SKIP | D_BVY) : 0u; break;
         case 0x6: d = D_OK | D_WVX; break;
         case 0x7: d = D_OK | D_WVX | D_VSADD; break;
         case 0x8:
@@ -322,7 +322,7 @@ void build_desc_table(uint32_t quirks, uint32_t out[kDescEntries]) {
             if (n >= 4 || ((quirks & OCTAX_Q_VF_RESET) && n >= 1)) d |= D_WVF;
           }
           break;
-        case 0x9: d = n == 0 ? (D_OK | D_SKIPNE | D_BVY) : 0u; break;
+        case 0x9: d = n == 0 ? (D_OK | D_SKIP | D_SINV | D_BVY) : 0u; break;
         case 0xA: d = D_OK | D_INNN; break;
         case 0xB: d = D_OK | D_BJMP; break;
         case 0xC: d = D_OK | D_RND; break;
@@ -331,7 +331,7 @@ void build_desc_table(uint32_t quirks, uint32_t out[kDescEntries]) {
       out[(hi << 4) | n] = d;
     }
   struct { uint32_t op; uint32_t d; } ef[] = {
-      {0xE09E, D_SKIPKEY}, {0xE0A1, D_SKIPNKEY}, {0xF007, D_WVX | D_VSDT}, {0xF00A, D_WAIT},
+      {0xE09E, D_SKIP | D_SKEY}, {0xE0A1, D_SKIP | D_SKEY | D_SINV}, {0xF007, D_WVX | D_VSDT}, {0xF00A, D_WAIT},
       {0xF015, D_DTW},     {0xF018, D_STW},      {0xF01E, D_IADD},         {0xF029, D_IFONT},
       {0xF033, D_MEM},     {0xF055, D_MEM},      {0xF065, D_MEM}};
   for (auto &e : ef) out[desc_index(e.op)] = D_OK | D_YCHK | e.d | (((e.op >> 4) & 15u) << 28);

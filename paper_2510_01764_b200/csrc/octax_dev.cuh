@@ -20,8 +20,10 @@ constexpr uint32_t kStageBytes = kImageBytes + 4 * kDescEntries;  // image + dec
 // E/F entries carry the expected y nibble (bits 28..31, checked under D_YCHK): with
 // the injective nibble hash below, (hi, hash, y) determines the whole word.
 enum : uint32_t {
-  D_OK = 1u << 0, D_YCHK = 1u << 1, D_SKIPEQ = 1u << 2, D_SKIPNE = 1u << 3, D_BVY = 1u << 4,
-  D_SKIPKEY = 1u << 5, D_SKIPNKEY = 1u << 6, D_WVX = 1u << 7, D_WVF = 1u << 8, D_VSADD = 1u << 9,
+  // skips: D_SKIP = conditional skip; the condition is VX == (D_BVY ? VY : NN), or with
+  // D_SKEY "key VX & 15 is down"; D_SINV negates it (4XNN, 9XY0, EXA1)
+  D_OK = 1u << 0, D_YCHK = 1u << 1, D_SKIP = 1u << 2, D_SINV = 1u << 3, D_BVY = 1u << 4,
+  D_SKEY = 1u << 5, D_WVX = 1u << 7, D_WVF = 1u << 8, D_VSADD = 1u << 9,
   D_VSALU = 1u << 10, D_VSDT = 1u << 11, D_WAIT = 1u << 12, D_PCJ = 1u << 13, D_CALL = 1u << 14,
   D_BJMP = 1u << 15, D_INNN = 1u << 16, D_IADD = 1u << 17, D_IFONT = 1u << 18, D_DTW = 1u << 19,
   D_STW = 1u << 20, D_RND = 1u << 21, D_MEM = 1u << 22, D_DRAW = 1u << 23,

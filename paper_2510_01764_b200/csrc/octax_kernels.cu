@@ -144,7 +144,8 @@ __device__ __forceinline__ void put_rows(uint64_t *ob_env, uint32_t pl, uint32_t
 
 // ---------------------------------------------------------------- lane state
 struct Lane {
-  uint32_t pc, I, sp, dt, st, halted, keys, draw, episode;
+  uint32_t pc, I, sp, dt, st, halted, draw, episode;
+  uint32_t keys;    // held key mask, 16 bits replicated into both halves
   uint64_t dirty;   // copy-on-write mask: block b (64 B) of RAM lives in HBM
   uint8_t *ram;
   uint32_t stk_dirty;
@@ -365,9 +366,9 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   if (act && call) { sm.stk[L.sp * kBlock + tid] = (uint16_t)(pc + 2u); L.stk_dirty = 1; }
   // ---- skips: 3XNN 5XY0 on equal, 4XNN 9XY0 on not-equal, EX9E / EXA1 on key
   const bool eq = vx == (HAS(d, D_BVY) ? vy : nn);
-  const bool keyd = ((L.keys >> (vx & 15u)) & 1u) != 0u;
-  const bool skip = (HAS(d, D_SKIPEQ) && eq) || (HAS(d, D_SKIPNE) && !eq) ||
-                    (HAS(d, D_SKIPKEY) && keyd) || (HAS(d, D_SKIPNKEY) && !keyd);
+  // L.keys holds the 16-bit mask twice, so a wrapping funnel shift by VX tests key VX & 15
+  const bool keyd = (__funnelshift_r(L.keys, L.keys, vx) & 1u) != 0u;
+  const bool skip = HAS(d, D_SKIP) && ((HAS(d, D_SKEY) ? keyd : eq) != HAS(d, D_SINV));
   // ---- ALU 8XYn; flag written after the result (A15); VF-reset quirk folded into D_WVF
   const uint32_t s = (quirks & 1u) ? vy : vx;
   const bool sub5 = n == 5u, sub7 = n == 7u;
@@ -617,7 +618,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     if (active) {
       int32_t a = actions[env];
       if (a < 0 || (uint32_t)a >= p.n_actions) { err = 1; a = 0; }
-      L.keys = p.keymask[a];
+      L.keys = p.keymask[a] * 0x10001u;
     }
     // planes 0 (lanes 0-15, ring slot s0) and 1 (lanes 16-31, slot s1) of env `cur`:
     // one 16-B chunk per lane, loaded before a cycle and stored (in row order) after it
@@ -699,7 +700,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     if (resetting) power_on(sm, L, p, tid);
     __syncwarp();
     for (uint32_t seg = 0; seg < p.n_startup; ++seg) {
-      if (resetting) L.keys = p.startup_keys[seg];
+      if (resetting) L.keys = p.startup_keys[seg] * 0x10001u;
       run_frames<Q0>(sm, L, p, tid, lane, block0, gid, resetting, p.startup_frames[seg], wdirty);
     }
 

@@ -40,9 +40,14 @@ CONFIGS = [
     ("4", "target_shooter_level3", 262144, 0, "random"),
 ] + [("5", g, n, 0, "random") for g in ("pong_standin", "target_shooter_level3")
      for n in (1024, 4096, 16384, 65536, 262144, 1048576)]
+# SURVEY d.7 "mixed": the same rollouts after a 1,000-step random-action warm-up (every env
+# has diverged or been through a reset); "fresh" rows start 100 steps after reset
+MIXED = [("4", g, 262144, 0, "random") for g in ("pong_standin", "brix_standin", "target_shooter_level1",
+                                                 "target_shooter_level2", "target_shooter_level3")] + \
+        [("5", g, 1048576, 0, "random") for g in ("pong_standin", "target_shooter_level3")]
 
 
-def rollouts(game, n, obs_format, mode, reps, T=100):
+def rollouts(game, n, obs_format, mode, reps, T=100, warm=0):
     rom, spec = workloads.game(game, obs_format=obs_format)
     s = torch.cuda.Stream()
     env = OctaxEnv(rom, spec, n, workloads.ENV_SEED, stream=s)
@@ -53,6 +58,16 @@ def rollouts(game, n, obs_format, mode, reps, T=100):
                 env.gen_actions(workloads.ACTION_SEED, t, acts[t])
     s.synchronize()
     obs, rew, done = env.obs, env.reward, env.done
+    for t in range(warm):  # "mixed" (SURVEY d.7): diverge lanes with random actions first
+        with torch.cuda.stream(s):
+            env.gen_actions(workloads.ACTION_SEED ^ 0x5A5A, t, acts[0])
+        env.step_into(acts[0], obs, rew, done)
+    if warm:  # restore the rollout's first action row
+        with torch.cuda.stream(s):
+            if mode == "random":
+                env.gen_actions(workloads.ACTION_SEED, 0, acts[0])
+            else:
+                acts[0].zero_()
     times = []
     for r in range(reps + 1):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -77,9 +92,10 @@ def main():
     import bench
     rows = []
     cpu_cache = {}
-    for cid, game, n, fmt, mode in CONFIGS:
-        med, iqr = rollouts(game, n, fmt, mode, args.reps)
+    for cid, game, n, fmt, mode, warm in [c + (0,) for c in CONFIGS] + [c + (1000,) for c in MIXED]:
+        med, iqr = rollouts(game, n, fmt, mode, args.reps, warm=warm)
         row = {"config": cid, "game": game, "envs": n, "obs": "bool" if fmt else "packed", "actions": mode,
+               "protocol": "mixed" if warm else "fresh",
                "steps_per_s_median": med, "steps_per_s_iqr": iqr, "frames_per_s_median": 4 * med}
         if not args.no_cpu and game not in cpu_cache:
             one, _, _ = bench.oracle_throughput(game, 256, 100, procs=1)
@@ -93,10 +109,10 @@ def main():
     with open(args.out + ".json", "w") as f:
         json.dump({"device": dev, "protocol": "P:228, 1 warm-up + %d x 100-step rollouts" % args.reps,
                    "rows": rows}, f, indent=1)
-    lines = ["| config | game | envs | obs | actions | steps/s median | IQR | frames/s | oracle 1 core | oracle all cores (C) |",
-             "|---|---|---|---|---|---|---|---|---|---|"]
+    lines = ["| config | game | envs | obs | actions | protocol | steps/s median | IQR | frames/s | oracle 1 core | oracle all cores (C) |",
+             "|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
-        lines.append(f"| {r['config']} | {r['game']} | {r['envs']:,} | {r['obs']} | {r['actions']} | "
+        lines.append(f"| {r['config']} | {r['game']} | {r['envs']:,} | {r['obs']} | {r['actions']} | {r['protocol']} | "
                      f"{r['steps_per_s_median']:.4g} | {r['steps_per_s_iqr']:.3g} | {r['frames_per_s_median']:.4g} | "
                      f"{r.get('oracle_1core', float('nan')):.3g} | {r.get('oracle_all_cores', float('nan')):.3g} ({r.get('cores', '-')}) |")
     with open(args.out + ".md", "w") as f:
