@@ -23,7 +23,7 @@ enum : uint32_t {
   // skips: D_SKIP = conditional skip; the condition is VX == (D_BVY ? VY : NN), or with
   // D_SKEY "key VX & 15 is down"; D_SINV negates it (4XNN, 9XY0, EXA1)
   D_OK = 1u << 0, D_YCHK = 1u << 1, D_SKIP = 1u << 2, D_SINV = 1u << 3, D_BVY = 1u << 4,
-  D_SKEY = 1u << 5, D_WVX = 1u << 7, D_WVF = 1u << 8, D_VSADD = 1u << 9,
+  D_SKEY = 1u << 5, D_RARE = 1u << 6, D_WVX = 1u << 7, D_WVF = 1u << 8, D_VSADD = 1u << 9,
   D_VSALU = 1u << 10, D_VSDT = 1u << 11, D_WAIT = 1u << 12, D_PCJ = 1u << 13, D_CALL = 1u << 14,
   D_BJMP = 1u << 15, D_INNN = 1u << 16, D_IADD = 1u << 17, D_IFONT = 1u << 18, D_DTW = 1u << 19,
   D_STW = 1u << 20, D_RND = 1u << 21, D_MEM = 1u << 22, D_DRAW = 1u << 23,
@@ -46,9 +46,11 @@ inline uint32_t desc_index(uint32_t op) {
 // decision that depends on the word alone taken once (per handle, on the host, for all
 // 4096 PCs of the pristine image; on the device only for a PC in a dirty RAM block).
 //   .x = execution flags (D_* bits of D_EXEC, E_BAD / E_RET / E_CLS) | x << 28
-//   .y = kx | ky << 11 | nn << 24, with k* = 132 * register index (the smem V offset
-//        before the per-lane XOR, see VREG) -- kx addresses the register the word
-//        reads as "VX": V[x], or V0 for BNNN without the JUMP_VX quirk.
+//   .y = kx | ky << 11 | (sp delta + 1) << 22 | nn << 24, with k* = 132 * register
+//        index (the smem V offset before the per-lane XOR, see VREG) -- kx addresses the
+//        register the word reads as "VX": V[x], or V0 for BNNN without the JUMP_VX quirk;
+//        sp delta = +1 for 2NNN, -1 for 00EE (a new SP outside 0..16 is a stack fault).
+//   D_RARE marks the vote-gated classes (00E0, CXNN, FX33/55/65).
 constexpr uint32_t kDecEntries = 4097;  // PCs 0..0xFFF, entry 0x1000 (PC past memory) halts
 #ifdef __CUDACC__
 __host__ __device__
@@ -60,9 +62,11 @@ inline void make_entry(uint32_t op, const uint32_t *dtab, uint32_t quirks, uint3
   uint32_t f = bad ? E_BAD : (d & D_EXEC);
   if (op == 0x00EEu) f |= E_RET;
   if (op == 0x00E0u) f |= E_CLS;
+  if ((f & (E_CLS | D_RND | D_MEM)) != 0u) f |= D_RARE;
+  const uint32_t dsp = (f & E_RET) ? 0u : (f & D_CALL) ? 2u : 1u;
   const uint32_t rx = ((d & D_BJMP) != 0u && (quirks & 4u) == 0u) ? 0u : x;  // 4 = OCTAX_Q_JUMP_VX
   ex = f | (x << 28);
-  ey = (132u * rx) | ((132u * y) << 11) | (nn << 24);
+  ey = (132u * rx) | ((132u * y) << 11) | (dsp << 22) | (nn << 24);
 }
 
 // expression bytecode (postfix, evaluated with top-of-stack in a register)

@@ -350,9 +350,10 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     }
   }
   const uint32_t d = e.x, x = d >> 28, nn = e.y >> 24, n = nn & 15u, nnn = (x << 8) | nn;
-  const bool is_ret = HAS(d, E_RET), is_cls = HAS(d, E_CLS), call = HAS(d, D_CALL);
-  // ---- faults halt the lane (A17, A20)
-  const bool bad = HAS(d, E_BAD) || (is_ret && L.sp == 0u) || (call && L.sp == 16u);
+  const bool is_ret = HAS(d, E_RET), call = HAS(d, D_CALL);
+  const uint32_t nsp = L.sp + ((e.y >> 22) & 3u) - 1u;  // SP after 2NNN / 00EE
+  // ---- faults halt the lane (A17, A20): invalid word / PC past 0xFFE, stack over/underflow
+  const bool bad = HAS(d, E_BAD) || nsp > 16u;
   L.halted |= (uint32_t)(act && bad);
   act = act && !bad;
   // V[k] of this lane lives at k * 132 ^ tid (VREG); kx = V[x], or V0 for BNNN
@@ -362,7 +363,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   OCTAX_CHECK(!(act && call) || L.sp < 16u);
   OCTAX_CHECK(x < 16u && tid < kBlock);
   uint32_t ret_pc = 0;
-  if (act && is_ret) ret_pc = sm.stk[(L.sp - 1u) * kBlock + tid];
+  if (act && is_ret) ret_pc = sm.stk[nsp * kBlock + tid];
   if (act && call) { sm.stk[L.sp * kBlock + tid] = (uint16_t)(pc + 2u); L.stk_dirty = 1; }
   // ---- skips: 3XNN 5XY0 on equal, 4XNN 9XY0 on not-equal, EX9E / EXA1 on key
   const bool eq = vx == (HAS(d, D_BVY) ? vy : nn);
@@ -411,16 +412,16 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     L.pc = npc & 0xFFFFu;
     L.dec = __ldg(p.s.dec + min(L.pc, 0x1000u));  // next cycle's word, in flight meanwhile
     L.I = I2;
-    L.sp = L.sp + (uint32_t)call - (uint32_t)is_ret;
+    L.sp = nsp;
     L.dt = HAS(d, D_DTW) ? vx : L.dt;
     L.st = HAS(d, D_STW) ? vx : L.st;
   }
   const bool f33 = nn == 0x33u, f55 = nn == 0x55u;  // only meaningful under D_MEM
   // ---- vote-gated rare classes (one vote for CLS / CXNN / FX33-55-65 together)
-  const bool do_cls = act && is_cls;
+  if (__any_sync(kFull, act && HAS(d, D_RARE))) {
+  const bool do_cls = act && HAS(d, E_CLS);
   const bool do_rnd = act && HAS(d, D_RND);
   const bool do_mem = act && HAS(d, D_MEM);
-  if (__any_sync(kFull, do_cls || do_rnd || do_mem)) {
   if (__any_sync(kFull, do_cls)) {
     if (do_cls) {
 #pragma unroll
@@ -547,7 +548,8 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t block0 = (uint64_t)blockIdx.x * kBlock;
   const uint64_t env = block0 + tid;
-  const bool active = env < p.n;
+  const uint32_t nlive = p.n - block0 < (uint64_t)kBlock ? (uint32_t)(p.n - block0) : (uint32_t)kBlock;
+  const bool active = (uint32_t)tid < nlive;  // (32-bit: cheap to rematerialise)
   const uint64_t wbase = block0 + (uint64_t)warp * 32;
   const uint32_t h = p.head;
   OCTAX_CHECK(h < 4u && blockDim.x == (unsigned)kBlock);
