@@ -146,6 +146,9 @@ __device__ __forceinline__ void put_rows(uint64_t *ob_env, uint32_t pl, uint32_t
 struct Lane {
   uint32_t pc, I, sp, dt, st, halted, draw, episode;
   uint32_t keys;    // held key mask, 16 bits replicated into both halves
+  uint32_t wvm;     // descriptor bits that write VX this step: D_WVX, + D_WAIT if a key is held
+  uint32_t stay;    // D_WAIT if no key is held (FX0A re-executes), else 0
+  uint32_t kidx;    // lowest held key (FX0A result)
   uint64_t dirty;   // copy-on-write mask: block b (64 B) of RAM lives in HBM
   uint8_t *ram;
   uint32_t stk_dirty;
@@ -153,6 +156,14 @@ struct Lane {
 };
 
 #define VREG(k) sm.V[((k) << 7) + ((uint32_t)tid ^ ((uint32_t)(k) << 2))]
+
+// the key mask held for a step / startup segment and the per-step FX0A constants
+__device__ __forceinline__ void set_keys(Lane &L, uint32_t km) {
+  L.keys = km * 0x10001u;
+  L.wvm = km ? (D_WVX | D_WAIT) : D_WVX;
+  L.stay = km ? 0u : D_WAIT;
+  L.kidx = (uint32_t)(__ffs(km) - 1);
+}
 // Flag test written with a two-bit mask (kPad is never set in an entry): keeps the
 // compiler from lowering a single-bit test to shift + and + compare (one LOP3 instead).
 constexpr uint32_t kPad = 1u << 24;
@@ -182,7 +193,8 @@ __device__ __forceinline__ void power_on(Smem &sm, Lane &L, const StepParams &p,
   for (int k = 0; k < 16; ++k) sm.stk[k * kBlock + tid] = 0;
 #pragma unroll
   for (int r = 0; r < 32; ++r) sm.fb[tid * 32 + r] = 0;
-  L.pc = 0x200; L.I = 0; L.sp = 0; L.dt = 0; L.st = 0; L.halted = 0; L.keys = 0; L.draw = 0;
+  L.pc = 0x200; L.I = 0; L.sp = 0; L.dt = 0; L.st = 0; L.halted = 0; L.draw = 0;
+  set_keys(L, 0u);
   L.dirty = 0;
   L.dec = __ldg(p.s.dec + 0x200);
   L.stk_dirty = 1;
@@ -390,19 +402,19 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   r8 = (n == 0xEu) ? ((s << 1) & 255u) : r8;
   f8 = (n == 0xEu) ? (s >> 7) : f8;
   // ---- register writes
-  const bool wait = HAS(d, D_WAIT), nokey = L.keys == 0u;
+
   uint32_t nvx = nn;
   nvx = HAS(d, D_VSADD) ? ((vx + nn) & 255u) : nvx;
   nvx = HAS(d, D_VSALU) ? r8 : nvx;
   nvx = HAS(d, D_VSDT) ? L.dt : nvx;
-  nvx = wait ? (uint32_t)(__ffs(L.keys) - 1) : nvx;
-  if (act && (HAS(d, D_WVX) || (wait && !nokey))) sm.V[ax] = (uint8_t)nvx;
+  nvx = HAS(d, D_WAIT) ? L.kidx : nvx;
+  if (act && (d & L.wvm) != 0u) sm.V[ax] = (uint8_t)nvx;
   if (act && HAS(d, D_WVF)) VREG(15) = (uint8_t)f8;
   // ---- control flow and index / timer registers
   uint32_t npc = pc + (skip ? 4u : 2u);
   npc = HAS(d, D_PCJ) ? nnn : npc;  // 1NNN, 2NNN
   npc = is_ret ? ret_pc : npc;
-  npc = (wait && nokey) ? pc : npc;  // A16: FX0A re-executes while no key
+  npc = (d & L.stay) != 0u ? pc : npc;  // A16: FX0A re-executes while no key
   npc = HAS(d, D_BJMP) ? ((nnn + vx) & 0xFFFu) : npc;  // vx = V0 or V[x] (JUMP_VX quirk)
   uint32_t I2 = L.I;
   I2 = HAS(d, D_INNN) ? nnn : I2;
@@ -563,7 +575,8 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   if (tid == 0) stage_issue(sm, p.s.image, MODE == MODE_STEP ? ring_at(p, s2, block0) : nullptr);
 
   Lane L;
-  L.pc = 0x200; L.I = 0; L.sp = 0; L.dt = 0; L.st = 0; L.halted = 1; L.keys = 0; L.draw = 0; L.episode = 0;
+  L.pc = 0x200; L.I = 0; L.sp = 0; L.dt = 0; L.st = 0; L.halted = 1; L.draw = 0; L.episode = 0;
+  set_keys(L, 0u);
   L.dirty = 0; L.ram = p.s.ram; L.stk_dirty = 0;
   uint32_t steps = 0, prev = 0;
   int32_t ep_ret = 0;
@@ -620,7 +633,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     if (active) {
       int32_t a = actions[env];
       if (a < 0 || (uint32_t)a >= p.n_actions) { err = 1; a = 0; }
-      L.keys = p.keymask[a] * 0x10001u;
+      set_keys(L, p.keymask[a]);
     }
     // planes 0 (lanes 0-15, ring slot s0) and 1 (lanes 16-31, slot s1) of env `cur`:
     // one 16-B chunk per lane, loaded before a cycle and stored (in row order) after it
@@ -702,12 +715,12 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     if (resetting) power_on(sm, L, p, tid);
     __syncwarp();
     for (uint32_t seg = 0; seg < p.n_startup; ++seg) {
-      if (resetting) L.keys = p.startup_keys[seg] * 0x10001u;
+      if (resetting) set_keys(L, p.startup_keys[seg]);
       run_frames<Q0>(sm, L, p, tid, lane, block0, gid, resetting, p.startup_frames[seg], wdirty);
     }
 
     if (resetting) {
-      L.keys = 0;
+      set_keys(L, 0u);
       steps = 0;
       prev = eval(p.score, sm, L, tid);
       ep_ret = 0;
