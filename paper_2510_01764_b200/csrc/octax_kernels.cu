@@ -144,7 +144,8 @@ __device__ __forceinline__ void put_rows(uint64_t *ob_env, uint32_t pl, uint32_t
 
 // ---------------------------------------------------------------- lane state
 struct Lane {
-  uint32_t pc, I, sp, dt, st, halted, draw, episode;
+  uint32_t pc, sp, dt, st, halted, draw, episode;
+  uint32_t I;       // index register; only its low 16 bits are meaningful (FX1E wraps, A18)
   uint32_t keys;    // held key mask, 16 bits replicated into both halves
   uint32_t wvm;     // descriptor bits that write VX this step: D_WVX, + D_WAIT if a key is held
   uint32_t stay;    // D_WAIT if no key is held (FX0A re-executes), else 0
@@ -418,7 +419,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   npc = HAS(d, D_BJMP) ? ((nnn + vx) & 0xFFFu) : npc;  // vx = V0 or V[x] (JUMP_VX quirk)
   uint32_t I2 = L.I;
   I2 = HAS(d, D_INNN) ? nnn : I2;
-  I2 = HAS(d, D_IADD) ? ((I2 + vx) & 0xFFFFu) : I2;
+  I2 = HAS(d, D_IADD) ? (I2 + vx) : I2;  // 16-bit I kept modulo 2^32: users mask (A18)
   I2 = HAS(d, D_IFONT) ? (0x50u + 5u * (vx & 15u)) : I2;
   if (act) {
     L.pc = npc & 0xFFFFu;
@@ -509,7 +510,7 @@ __device__ __forceinline__ uint32_t eval(const Program &P, Smem &sm, const Lane 
     if (in.op <= X_ST) {  // push
       const uint32_t v = in.op == X_CONST ? in.imm
                        : in.op == X_V   ? (uint32_t)VREG(in.arg)
-                       : in.op == X_I   ? L.I
+                       : in.op == X_I   ? (L.I & 0xFFFFu)
                        : in.op == X_DT  ? L.dt : L.st;
 #pragma unroll
       for (int k = kMaxDepth - 1; k > 0; --k) st[k] = st[k - 1];

@@ -188,6 +188,34 @@ def test_set_get_state_roundtrip_random():
         assert np.array_equal(g.get_state(1), c)
 
 
+@pytest.mark.parametrize("quirks", [0, 31])
+def test_random_state_fuzz_parity(quirks):
+    """Arbitrary canonical states (any PC incl. odd and > 0xFFF, any stack contents, random
+    RAM = every block private, random display and history) on both sides, then 6 steps:
+    exercises the predecoded-table bounds, the dirty-RAM decode path and stack faults."""
+    rng = np.random.default_rng(11 + quirks)
+    rom, spec = workloads.game("brix_standin", quirks=quirks, max_episode_steps=0)
+    n = 64
+    g = _gpu_env(rom, spec, n, 9)
+    o = oracle.OracleEnv(rom, spec, n, 9)
+    for j in range(n):
+        c = rng.integers(0, 256, 5200, dtype=np.uint8)
+        c[20] = rng.integers(0, 17)
+        c[23] &= 1
+        c[76:80] = 0
+        if j % 4 == 0:   # PC near / past the end of memory
+            pc = int(rng.choice([0xFFC, 0xFFD, 0xFFE, 0xFFF, 0x1000, 0x1001, 0xFFFF]))
+            c[18], c[19] = pc & 255, pc >> 8
+        g.set_state(j, c)
+        o.set_state(j, c)
+    _assert_states(g, o, list(range(n)))
+    for t in range(6):
+        acts = workloads.gen.actions(12, t, n, 3)
+        gout, oout = _step_both(g, o, acts)
+        _assert_same(gout, oout, t)
+        _assert_states(g, o, list(range(n)))
+
+
 # ---------------------------------------------------------------- expressions
 EXPRS = ["V5", "(V14 // 10) - (V14 % 10)", "(V9 == 0) | (V12 >= 0x3E)", "V1 == 2",
          "mem[I] + mem[I + 1] * 256", "-V3 ^ ~V4", "V1 << V2 | V3 >> V4", "V1 / V2 + V3 % V4",
