@@ -46,8 +46,8 @@ inline uint32_t desc_index(uint32_t op) {
 // decision that depends on the word alone taken once (per handle, on the host, for all
 // 4096 PCs of the pristine image; on the device only for a PC in a dirty RAM block).
 //   .x = execution flags (D_* bits of D_EXEC, E_BAD / E_RET / E_CLS) | x << 28
-//   .y = kx | ky << 11 | (sp delta + 1) << 22 | nn << 24, with k* = 132 * register
-//        index (the smem V offset before the per-lane XOR, see VREG) -- kx addresses the
+//   .y = kx | ky << 11 | (sp delta + 1) << 22 | nn << 24, with k* = (k >> 2) << 7 | (k & 3)
+//        for register index k (its smem V offset within the lane's bank, see VREG) -- kx addresses the
 //        register the word reads as "VX": V[x], or V0 for BNNN without the JUMP_VX quirk;
 //        sp delta = +1 for 2NNN, -1 for 00EE (a new SP outside 0..16 is a stack fault).
 //   D_RARE marks the vote-gated classes (00E0, CXNN, FX33/55/65).
@@ -66,7 +66,8 @@ inline void make_entry(uint32_t op, const uint32_t *dtab, uint32_t quirks, uint3
   const uint32_t dsp = (f & E_RET) ? 0u : (f & D_CALL) ? 2u : 1u;
   const uint32_t rx = ((d & D_BJMP) != 0u && (quirks & 4u) == 0u) ? 0u : x;  // 4 = OCTAX_Q_JUMP_VX
   ex = f | (x << 28);
-  ey = (132u * rx) | ((132u * y) << 11) | (dsp << 22) | (nn << 24);
+  const uint32_t kx = ((rx >> 2) << 7) | (rx & 3u), ky = ((y >> 2) << 7) | (y & 3u);
+  ey = kx | (ky << 11) | (dsp << 22) | (nn << 24);
 }
 
 // expression bytecode (postfix, evaluated with top-of-stack in a register)

@@ -51,7 +51,7 @@ struct __align__(128) Smem {
   uint8_t img[kImageBytes];                  // pristine image (TMA destination) ...
   uint32_t dtab[kDescEntries];               // ... immediately followed by the decode table
   uint64_t fb[kBlock * 32];                  // framebuffer rows, bit 63-x = pixel x, swizzled
-  uint8_t V[16 * kBlock];                    // V[k] of env t at k*128 + (t ^ 4k): bank (t>>2)^k
+  uint8_t V[16 * kBlock];                    // V[k] of env t: its own bank (see vbase / VREG)
   uint16_t stk[16 * kBlock];                 // stk[k*kBlock + tid]
   uint32_t dprm[kBlock / 32][32];            // DXYN owner params (x0 | y0 << 6 | base << 11)
   uint8_t down[kBlock / 32][32];             // DXYN item -> owner lane map
@@ -156,7 +156,13 @@ struct Lane {
   uint2 dec;        // predecoded word at pc, loaded one cycle ahead (latency hidden)
 };
 
-#define VREG(k) sm.V[((k) << 7) + ((uint32_t)tid ^ ((uint32_t)(k) << 2))]
+// V[k] of CTA lane tid: warp w's 32 lanes x 16 registers occupy 512 B, register k of
+// lane l at word 32 * (k >> 2) + l, byte k & 3 -- every lane's registers sit in its own
+// bank, so any per-lane mix of register indices is conflict free.
+__device__ __forceinline__ uint32_t vbase(int tid) {
+  return (((uint32_t)tid >> 5) << 9) | (((uint32_t)tid & 31u) << 2);
+}
+#define VREG(k) sm.V[vbase(tid) | (((uint32_t)(k) >> 2) << 7) | ((uint32_t)(k) & 3u)]
 
 // the key mask held for a step / startup segment and the per-step FX0A constants
 __device__ __forceinline__ void set_keys(Lane &L, uint32_t km) {
@@ -189,7 +195,7 @@ __device__ __forceinline__ void wr(const Smem &sm, Lane &L, uint32_t a, uint32_t
 
 __device__ __forceinline__ void power_on(Smem &sm, Lane &L, const StepParams &p, int tid) {
 #pragma unroll
-  for (int k = 0; k < 16; ++k) VREG(k) = 0;
+  for (int j = 0; j < 4; ++j) *reinterpret_cast<uint32_t *>(&sm.V[vbase(tid) | (j << 7)]) = 0u;
 #pragma unroll
   for (int k = 0; k < 16; ++k) sm.stk[k * kBlock + tid] = 0;
 #pragma unroll
@@ -369,8 +375,8 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   const bool bad = HAS(d, E_BAD) || nsp > 16u;
   L.halted |= (uint32_t)(act && bad);
   act = act && !bad;
-  // V[k] of this lane lives at k * 132 ^ tid (VREG); kx = V[x], or V0 for BNNN
-  const uint32_t ax = (e.y & 0x7FFu) ^ (uint32_t)tid, vx = sm.V[ax], vy = sm.V[((e.y >> 11) & 0x7FFu) ^ (uint32_t)tid];
+  // V[k] of this lane lives at vbase | voff(k) (VREG); kx = V[x], or V0 for BNNN
+  const uint32_t vb = vbase(tid), ax = (e.y & 0x7FFu) | vb, vx = sm.V[ax], vy = sm.V[((e.y >> 11) & 0x7FFu) | vb];
   // ---- stack
   OCTAX_CHECK(!(act && is_ret) || (L.sp >= 1u && L.sp <= 16u));
   OCTAX_CHECK(!(act && call) || L.sp < 16u);
@@ -586,7 +592,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     uint4 v = p.s.regs[env];
     uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int k = 0; k < 16; ++k) VREG(k) = (uint8_t)(w[k >> 2] >> (8 * (k & 3)));
+    for (int j = 0; j < 4; ++j) *reinterpret_cast<uint32_t *>(&sm.V[vbase(tid) | (j << 7)]) = w[j];
     uint4 c = p.s.ctrl[env];
     L.pc = c.x & 0xFFFFu; L.I = c.x >> 16;
     L.sp = c.y & 255u; L.dt = (c.y >> 8) & 255u; L.st = (c.y >> 16) & 255u; L.halted = c.y >> 24;
@@ -771,7 +777,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   if (active) {
     uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int k = 0; k < 16; ++k) w[k >> 2] |= (uint32_t)VREG(k) << (8 * (k & 3));
+    for (int j = 0; j < 4; ++j) w[j] = *reinterpret_cast<const uint32_t *>(&sm.V[vbase(tid) | (j << 7)]);
     p.s.regs[env] = make_uint4(w[0], w[1], w[2], w[3]);
     p.s.ctrl[env] = make_uint4(L.pc | (L.I << 16), L.sp | (L.dt << 8) | (L.st << 16) | (L.halted << 24),
                                L.draw, L.episode);
