@@ -27,9 +27,10 @@ enum : uint32_t {
   D_VSALU = 1u << 10, D_VSDT = 1u << 11, D_WAIT = 1u << 12, D_PCJ = 1u << 13, D_CALL = 1u << 14,
   D_BJMP = 1u << 15, D_INNN = 1u << 16, D_IADD = 1u << 17, D_IFONT = 1u << 18, D_DTW = 1u << 19,
   D_STW = 1u << 20, D_RND = 1u << 21, D_MEM = 1u << 22, D_DRAW = 1u << 23,
-  // predecoded-entry only (never in the descriptor table)
-  E_BAD = 1u << 25, E_RET = 1u << 26, E_CLS = 1u << 27,
-  D_EXEC = 0x00FFFFFCu  // descriptor bits that carry over into an entry
+  // predecoded-entry only (never in the descriptor table): the skip truth table (bit
+  // 1 + i = skip when i = [VX == operand] | [key VX down] << 1), VY-operand flag, faults
+  E_SKL = 0xFu << 1, E_BVY = 1u << 5, E_BAD = 1u << 25, E_RET = 1u << 26, E_CLS = 1u << 27,
+  D_EXEC = 0x00FFFFC0u  // descriptor bits that carry over into an entry unchanged
 };
 
 // hi << 4 | low nibble; for EXnn / FXnn the nibble is (n - 2y) & 15, which is
@@ -45,11 +46,12 @@ inline uint32_t desc_index(uint32_t op) {
 // Predecoded instruction: what the core needs from the 16-bit word at a PC, with every
 // decision that depends on the word alone taken once (per handle, on the host, for all
 // 4096 PCs of the pristine image; on the device only for a PC in a dirty RAM block).
-//   .x = execution flags (D_* bits of D_EXEC, E_BAD / E_RET / E_CLS) | x << 28
-//   .y = kx | ky << 11 | (sp delta + 1) << 22 | nn << 24, with k* = (k >> 2) << 7 | (k & 3)
-//        for register index k (its smem V offset within the lane's bank, see VREG) -- kx addresses the
-//        register the word reads as "VX": V[x], or V0 for BNNN without the JUMP_VX quirk;
-//        sp delta = +1 for 2NNN, -1 for 00EE (a new SP outside 0..16 is a stack fault).
+//   .x = execution flags: D_* bits of D_EXEC, E_SKL / E_BVY (skips), E_BAD / E_RET / E_CLS
+//   .y = kx | ky << 9 | (sp delta + 1) << 18 | nnn << 20 (nn at bits 20..27, x 28..31), with
+//        k* = (k >> 2) << 7 | (k & 3) for register index k (its smem V offset within the
+//        lane's bank, see VREG) -- kx addresses the register the word reads as "VX":
+//        V[x], or V0 for BNNN without the JUMP_VX quirk; sp delta = +1 for 2NNN, -1 for
+//        00EE (a new SP outside 0..16 is a stack fault).
 //   D_RARE marks the vote-gated classes (00E0, CXNN, FX33/55/65).
 constexpr uint32_t kDecEntries = 4097;  // PCs 0..0xFFF, entry 0x1000 (PC past memory) halts
 #ifdef __CUDACC__
@@ -60,14 +62,19 @@ inline void make_entry(uint32_t op, const uint32_t *dtab, uint32_t quirks, uint3
   const uint32_t d = dtab[desc_index(op)];
   const bool bad = (d & D_OK) == 0u || ((d & D_YCHK) != 0u && y != (d >> 28));
   uint32_t f = bad ? E_BAD : (d & D_EXEC);
+  if (!bad && (d & D_SKIP) != 0u) {
+    const uint32_t lut = (d & D_SKEY) ? 0xCu : 0xAu;  // skip when the key is down / VX == operand
+    f |= ((d & D_SINV) ? (~lut & 0xFu) : lut) << 1;
+    if (d & D_BVY) f |= E_BVY;
+  }
   if (op == 0x00EEu) f |= E_RET;
   if (op == 0x00E0u) f |= E_CLS;
   if ((f & (E_CLS | D_RND | D_MEM)) != 0u) f |= D_RARE;
   const uint32_t dsp = (f & E_RET) ? 0u : (f & D_CALL) ? 2u : 1u;
   const uint32_t rx = ((d & D_BJMP) != 0u && (quirks & 4u) == 0u) ? 0u : x;  // 4 = OCTAX_Q_JUMP_VX
-  ex = f | (x << 28);
+  ex = f;
   const uint32_t kx = ((rx >> 2) << 7) | (rx & 3u), ky = ((y >> 2) << 7) | (y & 3u);
-  ey = kx | (ky << 11) | (dsp << 22) | (nn << 24);
+  ey = kx | (ky << 9) | (dsp << 18) | (nn << 20) | (x << 28);
 }
 
 // expression bytecode (postfix, evaluated with top-of-stack in a register)

@@ -368,15 +368,15 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
       if (slow) make_entry((rd(sm, L, pc) << 8) | rd(sm, L, pc + 1), sm.dtab, quirks, e.x, e.y);
     }
   }
-  const uint32_t d = e.x, x = d >> 28, nn = e.y >> 24, n = nn & 15u, nnn = (x << 8) | nn;
+  const uint32_t d = e.x, nnn = e.y >> 20, nn = nnn & 255u, n = nnn & 15u, x = nnn >> 8;
   const bool is_ret = HAS(d, E_RET), call = HAS(d, D_CALL);
-  const uint32_t nsp = L.sp + ((e.y >> 22) & 3u) - 1u;  // SP after 2NNN / 00EE
+  const uint32_t nsp = L.sp + ((e.y >> 18) & 3u) - 1u;  // SP after 2NNN / 00EE
   // ---- faults halt the lane (A17, A20): invalid word / PC past 0xFFE, stack over/underflow
   const bool bad = HAS(d, E_BAD) || nsp > 16u;
   L.halted |= (uint32_t)(act && bad);
   act = act && !bad;
   // V[k] of this lane lives at vbase | voff(k) (VREG); kx = V[x], or V0 for BNNN
-  const uint32_t vb = vbase(tid), ax = (e.y & 0x7FFu) | vb, vx = sm.V[ax], vy = sm.V[((e.y >> 11) & 0x7FFu) | vb];
+  const uint32_t vb = vbase(tid), ax = (e.y & 0x1FFu) | vb, vx = sm.V[ax], vy = sm.V[((e.y >> 9) & 0x1FFu) | vb];
   // ---- stack
   OCTAX_CHECK(!(act && is_ret) || (L.sp >= 1u && L.sp <= 16u));
   OCTAX_CHECK(!(act && call) || L.sp < 16u);
@@ -385,10 +385,12 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   if (act && is_ret) ret_pc = sm.stk[nsp * kBlock + tid];
   if (act && call) { sm.stk[L.sp * kBlock + tid] = (uint16_t)(pc + 2u); L.stk_dirty = 1; }
   // ---- skips: 3XNN 5XY0 on equal, 4XNN 9XY0 on not-equal, EX9E / EXA1 on key
-  const bool eq = vx == (HAS(d, D_BVY) ? vy : nn);
-  // L.keys holds the 16-bit mask twice, so a wrapping funnel shift by VX tests key VX & 15
-  const bool keyd = (__funnelshift_r(L.keys, L.keys, vx) & 1u) != 0u;
-  const bool skip = HAS(d, D_SKIP) && ((HAS(d, D_SKEY) ? keyd : eq) != HAS(d, D_SINV));
+  // index i = [VX == operand] | [key VX & 15 down] << 1 into the entry's skip truth table;
+  // L.keys holds the 16-bit mask twice, so a wrapping funnel shift by VX - 1 puts key
+  // VX & 15 at bit 1
+  const uint32_t eq01 = vx == (HAS(d, E_BVY) ? vy : nn) ? 1u : 0u;
+  const uint32_t sidx = (__funnelshift_r(L.keys, L.keys, vx - 1u) & 2u) | eq01;
+  const uint32_t skip2 = (d >> sidx) & 2u;  // 2 if the next word is skipped
   // ---- ALU 8XYn; flag written after the result (A15); VF-reset quirk folded into D_WVF
   const uint32_t s = (quirks & 1u) ? vy : vx;
   const bool sub5 = n == 5u, sub7 = n == 7u;
@@ -402,23 +404,23 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   r8 = (n == 2u) ? (vx & vy) : r8;
   r8 = (n == 3u) ? (vx ^ vy) : r8;
   const bool add = (n == 4u) || sub5 || sub7;
-  r8 = add ? (sum & 255u) : r8;
+  r8 = add ? sum : r8;  // r8 / nvx are stored as bytes: no masking
   f8 = add ? (sum >> 8) : f8;
   r8 = (n == 6u) ? (s >> 1) : r8;
   f8 = (n == 6u) ? (s & 1u) : f8;
-  r8 = (n == 0xEu) ? ((s << 1) & 255u) : r8;
+  r8 = (n == 0xEu) ? (s << 1) : r8;
   f8 = (n == 0xEu) ? (s >> 7) : f8;
   // ---- register writes
 
   uint32_t nvx = nn;
-  nvx = HAS(d, D_VSADD) ? ((vx + nn) & 255u) : nvx;
+  nvx = HAS(d, D_VSADD) ? (vx + nn) : nvx;
   nvx = HAS(d, D_VSALU) ? r8 : nvx;
   nvx = HAS(d, D_VSDT) ? L.dt : nvx;
   nvx = HAS(d, D_WAIT) ? L.kidx : nvx;
   if (act && (d & L.wvm) != 0u) sm.V[ax] = (uint8_t)nvx;
   if (act && HAS(d, D_WVF)) VREG(15) = (uint8_t)f8;
   // ---- control flow and index / timer registers
-  uint32_t npc = pc + (skip ? 4u : 2u);
+  uint32_t npc = pc + 2u + skip2;
   npc = HAS(d, D_PCJ) ? nnn : npc;  // 1NNN, 2NNN
   npc = is_ret ? ret_pc : npc;
   npc = (d & L.stay) != 0u ? pc : npc;  // A16: FX0A re-executes while no key
