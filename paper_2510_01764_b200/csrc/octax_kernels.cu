@@ -212,7 +212,7 @@ __device__ __forceinline__ void power_on(Smem &sm, Lane &L, const StepParams &p,
 // with 4 ballots (counts are 4-bit), owners publish (lane, params) into a per-warp
 // smem map at their start item, and each item finds its owner as the highest
 // start bit at or below it (one REDUX.OR + FLO), so a pass costs no shuffle chain.
-__device__ __forceinline__ void draw_coop(Smem &sm, const Lane &L, const StepParams &p, int tid, int lane,
+__device__ __noinline__ void draw_coop(Smem &sm, const Lane &L, const StepParams &p, int tid, int lane,
                                           uint64_t block0, bool do_draw, uint32_t x0, uint32_t y0, uint32_t base,
                                           uint32_t n, bool vfw, uint32_t quirks) {
   const bool wrap = (quirks & 8u) != 0;
