@@ -145,6 +145,7 @@ __device__ __forceinline__ void put_rows(uint64_t *ob_env, uint32_t pl, uint32_t
 // ---------------------------------------------------------------- lane state
 struct Lane {
   uint32_t pc, sp, dt, st, halted, draw, episode;
+  bool run;         // inside a cycle loop: this lane participates and has not halted
   uint32_t I;       // index register; only its low 16 bits are meaningful (FX1E wraps, A18)
   uint32_t keys;    // held key mask, 16 bits replicated into both halves
   uint32_t wvm;     // descriptor bits that write VX this step: D_WVX, + D_WAIT if a key is held
@@ -356,7 +357,7 @@ template <bool Q0>
 __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, int tid, int lane, uint64_t block0,
                                       uint32_t gid, bool part, bool &wdirty) {
   const uint32_t quirks = Q0 ? 0u : p.quirks;  // Q0: modern profile specialisation
-  bool act = part & (L.halted == 0u);
+  bool act = L.run;  // = part && !halted, maintained by the cycle loops
   const uint32_t pc = L.pc;
   // ---- fetch + decode: the predecoded word at PC (L1-resident table, loaded at the end
   //      of the previous cycle; PCs past 0xFFE halt through the table).  Slow path: PC in
@@ -373,8 +374,8 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   const uint32_t nsp = L.sp + ((e.y >> 18) & 3u) - 1u;  // SP after 2NNN / 00EE
   // ---- faults halt the lane (A17, A20): invalid word / PC past 0xFFE, stack over/underflow
   const bool bad = HAS(d, E_BAD) || nsp > 16u;
-  L.halted |= (uint32_t)(act && bad);
   act = act && !bad;
+  L.run = act;
   // V[k] of this lane lives at vbase | voff(k) (VREG); kx = V[x], or V0 for BNNN
   const uint32_t vb = vbase(tid), ax = (e.y & 0x1FFu) | vb, vx = sm.V[ax], vy = sm.V[((e.y >> 9) & 0x1FFu) | vb];
   // ---- stack
@@ -497,13 +498,15 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
 template <bool Q0>
 __device__ __forceinline__ void run_frames(Smem &sm, Lane &L, const StepParams &p, int tid, int lane, uint64_t block0,
                                            uint32_t gid, bool part, uint32_t frames, bool &wdirty) {
+  L.run = part && !L.halted;
   for (uint32_t f = 0; f < frames; ++f) {
     for (uint32_t k = 0; k < p.ipf; ++k) cycle<Q0>(sm, L, p, tid, lane, block0, gid, part, wdirty);
-    if (part && !L.halted) {
+    if (L.run) {
       L.dt -= (L.dt != 0u);
       L.st -= (L.st != 0u);
     }
   }
+  if (part) L.halted = !L.run;
 }
 
 // Postfix bytecode evaluator (uniform control flow: every lane runs the same
@@ -649,6 +652,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     const uint4 *rsrc = reinterpret_cast<const uint4 *>(ring_at(p, hh ? s1 : s0, wbase) + l2);
     uint64_t *odst = obs64 + wbase * 128 + hh * 32;
     int cur = sf ? ne : 0;
+    L.run = active && !L.halted;
     const uint4 *rp = rsrc + cur * 16;  // env `cur`'s chunk and obs row block, advanced per copy
     uint64_t *opl = odst + cur * 128;
     for (uint32_t f = 0; f < p.frame_skip; ++f) {
@@ -664,7 +668,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
           opl += 128;
         }
       }
-      if (active && !L.halted) {
+      if (L.run) {
         L.dt -= (L.dt != 0u);
         L.st -= (L.st != 0u);
       }
@@ -677,6 +681,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     }
 #pragma unroll 4
     for (int e = cur; e < ne; ++e) put_rows(odst + e * 128, 0u, l2 ^ ((uint32_t)e & 15u), __ldcs(rsrc + e * 16));
+    if (active) L.halted = !L.run;
     if (active) {
       const uint32_t s = eval(p.score, sm, L, tid);
       const int32_t d = (int32_t)(s - prev);
