@@ -320,6 +320,7 @@ __device__ __forceinline__ void draw_lanes(Smem &sm, Lane &L, const StepParams &
 // warp's largest row count) publish packed parameters to a per-warp smem slot by rank;
 // lane r of group g XORs row r of drawer g, so all drawers cost one row step.  The
 // collision bits come back with one ballot.  dm = lanes with >= 1 row; DXY0 -> VF = 0.
+template <bool DIRTY>  // DIRTY: some lane of the warp has private RAM (sprite bytes may live in HBM)
 __device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepParams &p, int tid, int lane,
                                             uint64_t block0, uint32_t dm, uint32_t x0, uint32_t y0, uint32_t base,
                                             uint32_t nrows, uint32_t lg, bool wdirty, uint32_t quirks, bool vfw) {
@@ -334,13 +335,17 @@ __device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepP
   const uint32_t q = gv ? sm.dprm[warp][g] : 0u;
   const uint32_t own = q >> 27, oe = wl + own;
   uint64_t od = 0;
-  if (wdirty) od = __shfl_sync(kFull, L.dirty, own);
+  if (DIRTY) od = __shfl_sync(kFull, L.dirty, own);
   bool hit = false;
   if (gv && r < ((q >> 23) & 15u)) {
     const uint32_t ox = q & 63u, a = ((q >> 11) & 0xFFFu) + r;
     uint32_t byte = 0;
-    if (a <= 0xFFFu)
-      byte = ((od >> (a >> 6)) & 1ull) ? (uint32_t)p.s.ram[(block0 + oe) * 4096ull + a] : (uint32_t)sm.img[a];
+    if (DIRTY) {
+      if (a <= 0xFFFu)
+        byte = ((od >> (a >> 6)) & 1ull) ? (uint32_t)p.s.ram[(block0 + oe) * 4096ull + a] : (uint32_t)sm.img[a];
+    } else {
+      byte = a <= 0xFFFu ? (uint32_t)sm.img[a] : 0u;  // no global load on the common path
+    }
     const uint32_t yy = (((q >> 6) & 31u) + r) & 31u, q8 = ox & 0x38u;
     const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> (ox & 7u), 0, 0x4401);
     const uint64_t mk = wrap ? ((w << q8) | (q8 ? (w >> (64u - q8)) : 0ull)) : (w << q8);
@@ -485,7 +490,12 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     // many enough to beat maxr lane-parallel row steps (uniform choice)
     const uint32_t lg = maxr > 1u ? 32u - (uint32_t)__clz(maxr - 1u) : 0u;
     if (maxr >= 3u && (uint32_t)__popc(dm) <= (32u >> lg))
-      draw_groups(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, lg, wdirty, quirks, do_draw);
+    {
+      if (wdirty)
+        draw_groups<true>(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, lg, wdirty, quirks, do_draw);
+      else
+        draw_groups<false>(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, lg, wdirty, quirks, do_draw);
+    }
     else if (maxr <= kLaneDrawMax)
       draw_lanes(sm, L, p, tid, do_draw, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
     else
