@@ -132,6 +132,7 @@ __device__ __forceinline__ void fb_store_issue(const Smem &sm, uint64_t *dst) {
 
 // ring slot `slot` of handle-local env `e` (32 positions; position j holds row j ^ (e & 15))
 __device__ __forceinline__ uint64_t *ring_at(const StepParams &p, uint32_t slot, uint64_t e) {
+  OCTAX_CHECK(slot < 4u && e * 32u < p.s.ring_stride);
   return p.s.ring + (uint64_t)slot * p.s.ring_stride + e * 32u;
 }
 
@@ -349,6 +350,7 @@ __device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepP
     const uint32_t yy = (((q >> 6) & 31u) + r) & 31u, q8 = ox & 0x38u;
     const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> (ox & 7u), 0, 0x4401);
     const uint64_t mk = wrap ? ((w << q8) | (q8 ? (w >> (64u - q8)) : 0ull)) : (w << q8);
+    OCTAX_CHECK(oe < (uint32_t)kBlock && yy < 32u);
     uint64_t *row = &sm.fb[oe * 32u + (yy ^ (oe & 15u))];
     const uint64_t old = *row;
     *row = old ^ mk;
@@ -383,11 +385,13 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   L.run = act;
   // V[k] of this lane lives at vbase | voff(k) (VREG); kx = V[x], or V0 for BNNN
   const uint32_t vb = vbase(tid), ax = (e.y & 0x1FFu) | vb, vx = sm.V[ax], vy = sm.V[((e.y >> 9) & 0x1FFu) | vb];
+  OCTAX_CHECK(ax < 16u * kBlock && (((e.y >> 9) & 0x1FFu) | vb) < 16u * kBlock);
   // ---- stack
   OCTAX_CHECK(!(act && is_ret) || (L.sp >= 1u && L.sp <= 16u));
   OCTAX_CHECK(!(act && call) || L.sp < 16u);
   OCTAX_CHECK(x < 16u && tid < kBlock);
   uint32_t ret_pc = 0;
+  OCTAX_CHECK(!(act && is_ret) || nsp < 16u);
   if (act && is_ret) ret_pc = sm.stk[nsp * kBlock + tid];
   if (act && call) { sm.stk[L.sp * kBlock + tid] = (uint16_t)(pc + 2u); L.stk_dirty = 1; }
   // ---- skips: 3XNN 5XY0 on equal, 4XNN 9XY0 on not-equal, EX9E / EXA1 on key
