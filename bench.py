@@ -161,7 +161,7 @@ def run_reference(args):
         return 0
     envs_per_proc, steps_per_round = 256, 25
     vals, C, sample = oracle_throughput(args.game, envs_per_proc, steps_per_round,
-                                        rounds=args.warmup + args.steps)
+                                        procs=args.cpu_procs, rounds=args.warmup + args.steps)
     timed = sorted(vals[args.warmup:])
     v = timed[len(timed) // 2]
     out = {
@@ -255,6 +255,8 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-procs", type=int, default=None,
+                    help="--impl reference: oracle processes (default: one per host core)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 

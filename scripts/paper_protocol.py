@@ -8,12 +8,15 @@ run on the BASELINE.json configurations, plus the CPU oracle on the same box.
 Writes <out>.json and <out>.md (median and IQR of the 50 rollouts).  Each
 rollout = 100 octax_step launches with device-resident, pre-generated actions,
 timed with CUDA events on the env's stream after one untimed warm-up rollout.
+The oracle columns come from `bench.py --impl reference` (the one place besides
+the tests that runs the CPU oracle), on 1 process and on every host core.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -89,7 +92,12 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_paper_protocol"))
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
-    import bench
+    def oracle_ref(game, procs):
+        cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--game", game,
+               "--steps", "5", "--warmup", "1"] + (["--cpu-procs", str(procs)] if procs else [])
+        out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
+        d = json.loads(out.strip().splitlines()[-1])
+        return d["value"], d["cpu_baseline"]["cores"]
     rows = []
     cpu_cache = {}
     for cid, game, n, fmt, mode, warm in [c + (0,) for c in CONFIGS] + [c + (1000,) for c in MIXED]:
@@ -98,9 +106,9 @@ def main():
                "protocol": "mixed" if warm else "fresh",
                "steps_per_s_median": med, "steps_per_s_iqr": iqr, "frames_per_s_median": 4 * med}
         if not args.no_cpu and game not in cpu_cache:
-            one, _, _ = bench.oracle_throughput(game, 256, 100, procs=1)
-            allc, C, _ = bench.oracle_throughput(game, 256, 100)
-            cpu_cache[game] = (one[0], allc[0], C)
+            one, _ = oracle_ref(game, 1)
+            allc, C = oracle_ref(game, None)
+            cpu_cache[game] = (one, allc, C)
         if game in cpu_cache:
             row["oracle_1core"], row["oracle_all_cores"], row["cores"] = cpu_cache[game]
         rows.append(row)
