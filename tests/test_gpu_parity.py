@@ -442,3 +442,47 @@ def test_edge_rom_parity(name, quirks):
                 action_keys=list(range(16)), max_episode_steps=150, quirks=quirks)
     spec.update(over)
     _run_parity(edge_roms.rom(name), spec, 97, 160, 11 + quirks, 7, check_every=16)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("quirks", [0, 31])
+def test_decode_totality_gpu(quirks):
+    """SURVEY c.5: every one of the 65,536 instruction words executed once on the GPU, one
+    env per word, from random register / stack / timer state (PC = 0x300, one cycle per
+    step): halts exactly where the oracle halts and on no valid word, and the full
+    canonical state after the cycle matches the oracle for every env."""
+    from tests.test_oracle_pins import _valid_word
+    rng = np.random.default_rng(65536 + quirks)
+    rom, spec = workloads.game("brix_standin", quirks=quirks, frame_skip=1, instructions_per_frame=1,
+                               max_episode_steps=0, terminated="0", score="V0 + VF * 256 + I")
+    n = 65536
+    g = _gpu_env(rom, spec, n, 3)
+    o = oracle.OracleEnv(rom, spec, n, 3)
+    base = g.get_state(0)
+    sp = rng.integers(0, 17, n)
+    for w in range(n):
+        c = base.copy()
+        c[0:16] = rng.integers(0, 256, 16)
+        I = int(rng.integers(0, 0x1000))
+        c[16], c[17] = I & 255, I >> 8
+        c[18], c[19] = 0x00, 0x03                     # PC = 0x300
+        c[20] = sp[w]
+        c[21], c[22] = rng.integers(0, 256, 2)
+        c[24:56] = rng.integers(0, 256, 32)           # arbitrary return addresses
+        c[1104 + 0x300], c[1104 + 0x301] = w >> 8, w & 255
+        g.set_state(w, c)
+        o.set_state(w, c)
+    acts = workloads.gen.actions(17, 0, n, 3)
+    gout, oout = _step_both(g, o, acts)
+    _assert_same(gout, oout, 0)
+    done = oout[2].astype(bool)
+    ok_sp = (sp >= 1) & (sp <= 15)
+    valid = np.array([_valid_word(w) for w in range(n)])
+    assert not (done & valid & ok_sp).any()           # valid words never fault with a safe SP
+    assert done[~valid].all()                         # invalid words always halt
+    for lo in range(0, n, 4096):
+        ids = list(range(lo, lo + 4096))
+        gs = g.get_states(ids)
+        for j in ids:
+            if not np.array_equal(gs[j - lo], o.get_state(j)):
+                raise AssertionError(f"state differs for word {j:04X}")
