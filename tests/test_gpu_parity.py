@@ -275,6 +275,38 @@ def test_shard_invariance_gpu():
     assert np.array_equal(s[128:], hi.get_states(list(range(128))))
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_shard_invariance_r248_with_stats(world):
+    """SURVEY c.3 / §8(e): R = 2, 4, 8 ragged contiguous shards (dist.shard_total) of 1,003
+    global envs reproduce the single-handle run env by env (canonical state) and their
+    summed int64[4] statistics equal the single handle's (the all-reduce result)."""
+    from paper_2510_01764_b200 import dist
+    rom, spec = workloads.game("brix_standin", max_episode_steps=40)
+    total = 1003
+    full = _gpu_env(rom, spec, total, 8, 0)
+    parts = []
+    for r in range(world):
+        off, cnt = dist.shard_total(r, world, total)
+        parts.append((off, cnt, _gpu_env(rom, spec, cnt, 8, off)))
+    for t in range(60):
+        a = torch.empty(total, dtype=torch.int32, device="cuda")
+        full.gen_actions(31, t, a)
+        full.step(a)
+        for off, cnt, env in parts:
+            b = torch.empty(cnt, dtype=torch.int32, device="cuda")
+            env.gen_actions(31, t, b)            # keyed by global id: same actions
+            assert torch.equal(a[off:off + cnt], b)
+            env.step(b)
+    s = full.get_states(list(range(total)))
+    agg = np.zeros(4, np.int64)
+    for off, cnt, env in parts:
+        assert np.array_equal(s[off:off + cnt], env.get_states(list(range(cnt))))
+        st, rc = env.stats()
+        agg += st
+    fs, frc = full.stats()
+    assert np.array_equal(agg, fs) and fs[1] > 0
+
+
 def test_gen_actions_matches_oracle_generator():
     rom, spec = workloads.game("coverage")
     g = _gpu_env(rom, spec, 1000, 1, 5000)
