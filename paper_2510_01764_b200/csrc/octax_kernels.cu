@@ -46,6 +46,10 @@ namespace octax {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr uint32_t kLaneDrawMax = 8;  // rows: lane-parallel DXYN up to this, cooperative above
+// ceil(2^32 / m): lane / m = umulhi(lane, kRecip[m]) exactly for lane < 2^16 (m = 2..15)
+__constant__ uint32_t kRecip[16] = {0u, 0u, 0x80000000u, 0x55555556u, 0x40000000u, 0x33333334u,
+                                    0x2AAAAAABu, 0x24924925u, 0x20000000u, 0x1C71C71Du, 0x1999999Au,
+                                    0x1745D175u, 0x15555556u, 0x13B13B14u, 0x12492493u, 0x11111112u};
 
 struct __align__(128) Smem {
   uint8_t img[kImageBytes];                  // pristine image (TMA destination) ...
@@ -324,14 +328,15 @@ __device__ __forceinline__ void draw_lanes(Smem &sm, Lane &L, const StepParams &
 template <bool DIRTY>  // DIRTY: some lane of the warp has private RAM (sprite bytes may live in HBM)
 __device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepParams &p, int tid, int lane,
                                             uint64_t block0, uint32_t dm, uint32_t x0, uint32_t y0, uint32_t base,
-                                            uint32_t nrows, uint32_t lg, bool wdirty, uint32_t quirks, bool vfw) {
+                                            uint32_t nrows, uint32_t m, bool wdirty, uint32_t quirks, bool vfw) {
   const bool wrap = (quirks & 8u) != 0;
   const uint32_t warp = (uint32_t)tid >> 5, wl = (uint32_t)tid & ~31u;
   const bool mine = ((dm >> lane) & 1u) != 0u;
   const uint32_t rank = (uint32_t)__popc(dm & ((1u << lane) - 1u));
   if (mine) sm.dprm[warp][rank] = x0 | (y0 << 6) | (base << 11) | (nrows << 23) | ((uint32_t)lane << 27);
   __syncwarp();
-  const uint32_t g = (uint32_t)lane >> lg, r = (uint32_t)lane & ((1u << lg) - 1u);
+  // group g = lane / m, row r = lane % m (m = the warp's largest row count, 3..15)
+  const uint32_t g = __umulhi((uint32_t)lane, kRecip[m]), r = (uint32_t)lane - g * m;
   const bool gv = g < (uint32_t)__popc(dm);
   const uint32_t q = gv ? sm.dprm[warp][g] : 0u;
   const uint32_t own = q >> 27, oe = wl + own;
@@ -357,7 +362,28 @@ __device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepP
     hit = (old & mk) != 0ull;
   }
   const uint32_t hb = __ballot_sync(kFull, hit);
-  if (vfw) VREG(15) = (uint8_t)(mine && ((hb >> (rank << lg)) & ((1u << (1u << lg)) - 1u)) != 0u);
+  if (vfw) VREG(15) = (uint8_t)(mine && ((hb >> (rank * m)) & ((1u << m) - 1u)) != 0u);
+}
+
+// DXYN when no lane of the warp draws more than one row (a 1-row sprite, or clipped at
+// the bottom): one row step, no sprite-word realignment.
+template <bool DIRTY>
+__device__ __forceinline__ void draw_one(Smem &sm, const Lane &L, int tid, bool draws, uint32_t x0, uint32_t y0,
+                                         uint32_t base, uint32_t quirks, bool vfw) {
+  bool hit = false;
+  if (draws) {
+    uint32_t byte;
+    if (DIRTY) byte = rd(sm, L, base);
+    else byte = sm.img[base];
+    const uint32_t q8 = x0 & 0x38u;
+    const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> (x0 & 7u), 0, 0x4401);
+    const uint64_t mk = (quirks & 8u) ? ((w << q8) | (q8 ? (w >> (64u - q8)) : 0ull)) : (w << q8);
+    uint64_t *row = &sm.fb[(uint32_t)tid * 32u + (y0 ^ ((uint32_t)tid & 15u))];
+    const uint64_t old = *row;
+    *row = old ^ mk;
+    hit = (old & mk) != 0ull;
+  }
+  if (vfw) VREG(15) = (uint8_t)hit;
 }
 
 template <bool Q0>
@@ -490,17 +516,19 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     const uint32_t nrows = do_draw ? (((quirks & 8u) != 0u) ? n : min(n, 32u - y0)) : 0u;
     const uint32_t maxr = __reduce_max_sync(kFull, nrows);
     const uint32_t dm = __ballot_sync(kFull, nrows != 0u);
-    // one grouped pass (groups of 2^lg >= maxr lanes) when the drawers fit and rows are
-    // many enough to beat maxr lane-parallel row steps (uniform choice)
-    const uint32_t lg = maxr > 1u ? 32u - (uint32_t)__clz(maxr - 1u) : 0u;
-    if (maxr >= 3u && (uint32_t)__popc(dm) <= (32u >> lg))
+    // one grouped pass (groups of maxr lanes, 32 / maxr drawers) when the drawers fit and
+    // rows are many enough to beat maxr lane-parallel row steps (uniform choice)
+    if (maxr >= 3u && (uint32_t)__popc(dm) <= __umulhi(32u, kRecip[maxr]))
     {
       if (wdirty)
-        draw_groups<true>(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, lg, wdirty, quirks, do_draw);
+        draw_groups<true>(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
       else
-        draw_groups<false>(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, lg, wdirty, quirks, do_draw);
+        draw_groups<false>(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
     }
-    else if (maxr <= kLaneDrawMax)
+    else if (maxr == 1u) {
+      if (wdirty) draw_one<true>(sm, L, tid, nrows != 0u, vx & 63u, y0, L.I & 0xFFFu, quirks, do_draw);
+      else draw_one<false>(sm, L, tid, nrows != 0u, vx & 63u, y0, L.I & 0xFFFu, quirks, do_draw);
+    } else if (maxr <= kLaneDrawMax)
       draw_lanes(sm, L, p, tid, do_draw, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
     else
       draw_coop(sm, L, p, tid, lane, block0, do_draw, vx & 63u, y0, L.I & 0xFFFu, n, do_draw, quirks);
