@@ -9,22 +9,26 @@
 //     and "32 rows of one env"; the ring keeps the same swizzle); obs planes 0..2
 //     are written in row order with 16-B lane chunks, planes 0,1 streamed from
 //     the ring one env per VM cycle behind the interpreter;
+//   * fetch + decode is one L1 load of the word predecoded per handle at every PC
+//     (flags, skip truth table, stack delta, register offsets, NNN; make_entry in
+//     octax_dev.cuh), issued one VM cycle ahead; a PC in a dirty RAM block decodes
+//     on the device in a vote-gated slow path;
 //   * the interpreter loop (frame_skip x instructions_per_frame cycles,
 //     P:142-146) is WARP-UNIFORM: every lane runs the same straight-line,
 //     predicated core for the cheap opcode classes (no divergent dispatch
-//     tree), and the rare / heavy classes (DXYN, CXNN, 00E0, FX33/55/65,
-//     dirty-RAM fetch) are vote-gated blocks executed once per warp when any
-//     lane needs them;
-//   * DXYN is drawn cooperatively: the sprite rows of all drawing lanes are
-//     spread over the 32 lanes (prefix sum + binary search on shuffles), each
-//     lane XORs one 64-bit framebuffer row, and the collision flags are
-//     gathered with one __reduce_or_sync;
+//     tree), and the rare / heavy classes (DXYN, CXNN, 00E0, FX33/55/65) are
+//     vote-gated blocks executed once per warp when any lane needs them;
+//   * DXYN, chosen per warp and cycle from the drawing lanes' row
+//     counts: grouped (each drawer's rows spread over a group of lanes, one row
+//     step for up to 32 / maxr drawers, collisions from one ballot), single-row,
+//     lane-parallel (each lane its own rows), or cooperative (prefix-summed rows
+//     of all drawers over the 32 lanes);
 //   * score / termination bytecode -> reward, done; same-step
 //     auto-reset with startup segments (A10), also warp-uniform;
 //   * the epilogue bulk-stores the framebuffer block as the new ring slot and
 //     writes obs plane 3;
 //   * per-CTA integer episode statistics -> 4 int64 atomics per CTA.
-// Semantics follow DESIGN.md readings A1..A27; nothing here is shared with
+// Semantics follow DESIGN.md readings A1..A32; nothing here is shared with
 // the CPU oracle in oracle/.
 #include <cuda_runtime.h>
 
