@@ -70,22 +70,30 @@ def lockstep(game, warm=300, steps=40):
     for t in range(warm):
         o.step(workloads.gen.actions(workloads.ACTION_SEED, t, n, na))
     pcs, idle_lc, lc, tail, cyc = [], 0, 0, 0, 0
+    paths = {"grouped": 0, "single-row": 0, "lane-parallel": 0, "cooperative": 0}
     for t in range(warm, warm + steps):
         a = workloads.gen.actions(workloads.ACTION_SEED, t, n, na)
         keys = [0 if x == 0 else 1 << spec["action_keys"][x - 1] for x in a]
         for _ in range(fs):
             idle = np.zeros((ipf, n), bool)
             for k in range(ipf):
-                pc_k = []
+                pc_k, rows = [], []
                 for j in range(n):
                     f = oracle.canon_fields(o.get_state(j))
                     pc = int(f["PC"])
                     mem = f["mem"]
+                    word = (int(mem[pc]) << 8 | int(mem[pc + 1])) if pc < 0xFFF else 0
+                    if word >> 12 == 0xD and not f["halted"]:   # DXYN rows this cycle (clipped, A18)
+                        rows.append(min(word & 15, 32 - (int(f["V"][(word >> 4) & 15]) & 31)))
                     selfjump = pc < 0xFFF and (int(mem[pc]) << 8 | int(mem[pc + 1])) == (0x1000 | pc)
                     idle[k, j] = bool(f["halted"]) or selfjump or (pc in loops and int(f["DT"]) > 0)
                     pc_k.append(pc)
                     o.run_cycles(j, 1, keys[j])
                 pcs.append(len(set(pc_k)))
+                if rows:   # the kernel's per-warp DXYN choice (octax_kernels.cu, cycle())
+                    mx, kd = max(rows), sum(1 for r in rows if r)
+                    paths["grouped" if mx >= 3 and kd <= 32 // mx else "single-row" if mx == 1
+                          else "lane-parallel" if mx <= 8 else "cooperative"] += 1
             for j in range(n):
                 o.tick_timers(j)
             idle_lc += int(idle.sum())
@@ -99,7 +107,7 @@ def lockstep(game, warm=300, steps=40):
         # step-end bookkeeping (reward / termination / reset) is skipped here: the
         # run_cycles hooks do not evaluate expressions; 40 steps rarely end an episode
     return {"distinct_pcs": float(np.mean(pcs)), "idle_lane_cycles": idle_lc / lc,
-            "warp_skippable_cycles": tail / cyc}
+            "warp_skippable_cycles": tail / cyc, "draw_paths": {k: v / cyc for k, v in paths.items()}}
 
 
 def main():
@@ -108,14 +116,16 @@ def main():
     ap.add_argument("--games", nargs="*", default=GAMES)
     args = ap.parse_args()
     lines = ["| game | top classes (share of instructions) | DXYN/step | rows/DXYN | episodes/1k steps | "
-             "distinct PCs per warp-cycle | idle lane-cycles | all-32-idle frame-tail cycles |",
-             "|---|---|---|---|---|---|---|---|"]
+             "distinct PCs per warp-cycle | idle lane-cycles | all-32-idle frame-tail cycles | "
+             "warp-cycles by DXYN path (grouped / single-row / lane-parallel / cooperative) |",
+             "|---|---|---|---|---|---|---|---|---|"]
     for g in args.games:
         c, s = counters(g), lockstep(g)
         top = ", ".join(f"{k:X}: {100 * c['hist'][k]:.0f}%" for k in np.argsort(-c["hist"])[:6])
         lines.append(f"| {g} | {top} | {c['draws_per_step']:.2f} | {c['rows_per_draw']:.2f} | "
                      f"{c['episodes_per_1k']:.2f} | {s['distinct_pcs']:.1f} | {100 * s['idle_lane_cycles']:.1f}% | "
-                     f"{100 * s['warp_skippable_cycles']:.2f}% |")
+                     f"{100 * s['warp_skippable_cycles']:.2f}% | "
+                     + " / ".join(f"{100 * v:.0f}%" for v in s["draw_paths"].values()) + " |")
         print(lines[-1], flush=True)
     hdr = ("# Workload structure (oracle, random actions)\n\n"
            "Generated by `python -m tests.tools.workload_structure`.  Class = high nibble of the "
