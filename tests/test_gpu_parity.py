@@ -347,6 +347,37 @@ def test_full_size_sampled_parity():
     assert s[2] == n * T
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("game", ["pong_standin", "brix_standin", "target_shooter_level1",
+                                  "target_shooter_level2", "target_shooter_level3"])
+def test_config4_sampled_parity_1000_steps(game):
+    """SURVEY d.1 config 4 as specified: n = 262,144, T = 1,000 steps with device-generated
+    random actions; envs {0, 1, n/2, n-1} + 60 Philox-domain-2 ids gathered on device every
+    step and compared with one oracle instance each; final canonical states compared."""
+    rom, spec = workloads.game(game)
+    n, T = 262144, 1000
+    na = workloads.n_actions(spec)
+    g = _gpu_env(rom, spec, n, workloads.ENV_SEED)
+    a = torch.empty(n, dtype=torch.int32, device="cuda")
+    key = [workloads.ENV_SEED & 0xFFFFFFFF, workloads.ENV_SEED >> 32]
+    ids = [0, 1, n // 2, n - 1] + [oracle.philox4x32_10([k, 0, 0, 2], key)[0] % n for k in range(60)]
+    oracles = [oracle.OracleEnv(rom, spec, 1, workloads.ENV_SEED, gid) for gid in ids]
+    idx = torch.tensor(ids, device="cuda")
+    for t in range(T):
+        g.gen_actions(workloads.ACTION_SEED, t, a)
+        obs, rew, done = g.step(a)
+        go = obs.reshape(n, -1)[idx].cpu().numpy()
+        gr = rew[idx].cpu().numpy()
+        gd = done[idx].cpu().numpy()
+        for k, gid in enumerate(ids):
+            act = np.array([oracle.synthetic_action(workloads.ACTION_SEED, t, gid, na)], np.int32)
+            oo, orw, od, _, _ = oracles[k].step(act)
+            assert np.array_equal(go[k], oo[0]) and gr[k] == orw[0] and gd[k] == od[0], (t, gid)
+    st = g.get_states(ids)
+    for k in range(len(ids)):
+        assert np.array_equal(st[k], oracles[k].get_state(0)), ids[k]
+
+
 def test_cuda_graph_capture_matches_eager():
     """Steps captured in a CUDA graph (bench sweep mode) give the same states as eager launches."""
     from paper_2510_01764_b200 import OctaxEnv
