@@ -59,7 +59,8 @@ def build_variant(out: str, defines=()) -> str:
 
 
 if __name__ == "__main__":
-    if "--out" in sys.argv:
-        print(build_variant(sys.argv[sys.argv.index("--out") + 1]))
+    if "--out" in sys.argv:  # A/B variant: --out ab/x.so [-D NAME=VAL ...]
+        defs = [sys.argv[i + 1] for i, a in enumerate(sys.argv) if a == "-D"]
+        print(build_variant(sys.argv[sys.argv.index("--out") + 1], defs))
     else:
         print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

@@ -5,7 +5,14 @@
 
 namespace octax {
 
-constexpr int kBlock = 128;          // envs (threads) per CTA
+#ifndef OCTAX_BLOCK
+#define OCTAX_BLOCK 128
+#endif
+#ifndef OCTAX_MINB
+#define OCTAX_MINB 5
+#endif
+constexpr int kBlock = OCTAX_BLOCK;  // envs (threads) per CTA (a multiple of 32)
+constexpr int kMinBlocks = OCTAX_MINB;  // resident CTAs per SM the step kernel is built for
 constexpr int kFbStride = 33;        // u64 per env row block in smem (32 rows + 1 pad)
 constexpr int kMaxStartup = 32;
 constexpr int kMaxOps = 64;
@@ -53,7 +60,16 @@ inline uint32_t desc_index(uint32_t op) {
 //        V[x], or V0 for BNNN without the JUMP_VX quirk; sp delta = +1 for 2NNN, -1 for
 //        00EE (a new SP outside 0..16 is a stack fault).
 //   D_RARE marks the vote-gated classes (00E0, CXNN, FX33/55/65).
-constexpr uint32_t kDecEntries = 4097;  // PCs 0..0xFFF, entry 0x1000 (PC past memory) halts
+//   8XYn (D_VSALU): .y bits 24..31 (the x / high-nn fields, which the core does not read
+//   for 8XYn) hold the ALU operation one-hot (A_*), so the core selects the result with
+//   single-bit tests instead of comparing n; for 8XYE without the SHIFT_VY quirk the VY
+//   offset is VX's, so VX << 1 is the A_ADD of VX and VX.
+enum : uint32_t {
+  A_OR = 1u << 24, A_AND = 1u << 25, A_XOR = 1u << 26, A_ADD = 1u << 27,  // A_ADD: 8XY4, 8XYE
+  A_SUB = 1u << 28, A_RSUB = 1u << 29, A_SHR = 1u << 30,                   // 8XY5, 8XY7, 8XY6
+  A_SRCY = 1u << 31  // SHIFT_VY quirk: 8XY6 / 8XYE shift VY (never set for the modern profile)
+};
+constexpr uint32_t kDecEntries = 65536;  // every 16-bit PC: entries past 0xFFE halt (A17), so no clamp
 #ifdef __CUDACC__
 __host__ __device__
 #endif
@@ -73,8 +89,17 @@ inline void make_entry(uint32_t op, const uint32_t *dtab, uint32_t quirks, uint3
   const uint32_t dsp = (f & E_RET) ? 0u : (f & D_CALL) ? 2u : 1u;
   const uint32_t rx = ((d & D_BJMP) != 0u && (quirks & 4u) == 0u) ? 0u : x;  // 4 = OCTAX_Q_JUMP_VX
   ex = f;
-  const uint32_t kx = ((rx >> 2) << 7) | (rx & 3u), ky = ((y >> 2) << 7) | (y & 3u);
+  const uint32_t kx = ((rx >> 2) << 7) | (rx & 3u);
+  const uint32_t n = op & 15u, shy = quirks & 1u;  // 1 = OCTAX_Q_SHIFT_VY
+  const uint32_t ry = ((f & D_VSALU) != 0u && n == 0xEu && !shy) ? x : y;  // 8XYE: VX + VX
+  const uint32_t ky = ((ry >> 2) << 7) | (ry & 3u);
   ey = kx | (ky << 9) | (dsp << 18) | (nn << 20) | (x << 28);
+  if ((f & D_VSALU) != 0u) {
+    const uint32_t a = n == 1u ? A_OR : n == 2u ? A_AND : n == 3u ? A_XOR : n == 4u ? A_ADD
+                     : n == 5u ? A_SUB : n == 7u ? A_RSUB : n == 6u ? (A_SHR | (shy ? A_SRCY : 0u))
+                     : n == 0xEu ? (A_ADD | (shy ? A_SRCY : 0u)) : 0u;  // n == 0: VX = VY
+    ey = (ey & 0x00FFFFFFu) | a;
+  }
 }
 
 // expression bytecode (postfix, evaluated with top-of-stack in a register)

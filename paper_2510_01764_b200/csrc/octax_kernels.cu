@@ -186,6 +186,7 @@ __device__ __forceinline__ void set_keys(Lane &L, uint32_t km) {
 constexpr uint32_t kPad = 1u << 24;
 #define HAS(d, F) (((d) & ((F) | kPad)) != 0u)
 
+
 __device__ __forceinline__ uint32_t rd(const Smem &sm, const Lane &L, uint32_t a) {
   OCTAX_CHECK(a < 4096u);
   return ((L.dirty >> (a >> 6)) & 1ull) ? (uint32_t)L.ram[a] : (uint32_t)sm.img[a];
@@ -431,25 +432,20 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   const uint32_t eq01 = vx == (HAS(d, E_BVY) ? vy : nn) ? 1u : 0u;
   const uint32_t sidx = (__funnelshift_r(L.keys, L.keys, vx - 1u) & 2u) | eq01;
   const uint32_t skip2 = (d >> sidx) & 2u;  // 2 if the next word is skipped
-  // ---- ALU 8XYn; flag written after the result (A15); VF-reset quirk folded into D_WVF
-  const uint32_t s = (quirks & 1u) ? vy : vx;
-  const bool sub5 = n == 5u, sub7 = n == 7u;
-  const uint32_t sa = sub7 ? vy : vx;
-  uint32_t sb = vy;
-  sb = sub5 ? (vy ^ 255u) : sb;
-  sb = sub7 ? (vx ^ 255u) : sb;
-  const uint32_t sum = sa + sb + (uint32_t)(sub5 || sub7);
-  uint32_t r8 = vy, f8 = 0u;
-  r8 = (n == 1u) ? (vx | vy) : r8;
-  r8 = (n == 2u) ? (vx & vy) : r8;
-  r8 = (n == 3u) ? (vx ^ vy) : r8;
-  const bool add = (n == 4u) || sub5 || sub7;
-  r8 = add ? sum : r8;  // r8 / nvx are stored as bytes: no masking
-  f8 = add ? (sum >> 8) : f8;
-  r8 = (n == 6u) ? (s >> 1) : r8;
-  f8 = (n == 6u) ? (s & 1u) : f8;
-  r8 = (n == 0xEu) ? (s << 1) : r8;
-  f8 = (n == 0xEu) ? (s >> 7) : f8;
+  // ---- ALU 8XYn from the entry's one-hot operation (A_*); the flag is written after the
+  //      result (A15); VF-reset quirk folded into D_WVF (logic results have s8 >> 8 == 0)
+  const uint32_t ea = e.y;
+  const uint32_t sa = Q0 ? vx : ((ea & A_SRCY) ? vy : vx);  // shift source (SHIFT_VY quirk)
+  uint32_t s8 = vy;  // 8XY0
+  if (ea & A_OR) s8 = vx | vy;
+  if (ea & A_AND) s8 = vx & vy;
+  if (ea & A_XOR) s8 = vx ^ vy;
+  if (ea & A_ADD) s8 = sa + vy;          // 8XY4; 8XYE as VX + VX (or VY + VY)
+  if (ea & A_SUB) s8 = vx - vy + 256u;   // 8XY5: bit 8 = no borrow
+  if (ea & A_RSUB) s8 = vy - vx + 256u;  // 8XY7
+  uint32_t f8 = s8 >> 8;
+  if (ea & A_SHR) { s8 = sa >> 1; f8 = sa & 1u; }
+  const uint32_t r8 = s8;  // stored as a byte: no masking
   // ---- register writes
 
   uint32_t nvx = nn;
@@ -470,8 +466,8 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   I2 = HAS(d, D_IADD) ? (I2 + vx) : I2;  // 16-bit I kept modulo 2^32: users mask (A18)
   I2 = HAS(d, D_IFONT) ? (0x50u + 5u * (vx & 15u)) : I2;
   if (act) {
-    L.pc = npc & 0xFFFFu;
-    L.dec = __ldg(p.s.dec + min(L.pc, 0x1000u));  // next cycle's word, in flight meanwhile
+    L.pc = npc;  // < 2^16: PC <= 0xFFE when active, stack entries are u16, BNNN masks
+    L.dec = __ldg(p.s.dec + L.pc);  // next cycle's word, in flight meanwhile
     L.I = I2;
     L.sp = nsp;
     L.dt = HAS(d, D_DTW) ? vx : L.dt;
@@ -609,7 +605,7 @@ __device__ __forceinline__ uint32_t eval(const Program &P, Smem &sm, const Lane 
 
 // ---------------------------------------------------------------- the step kernel
 template <int MODE, bool Q0>
-__global__ void __launch_bounds__(kBlock, 5)
+__global__ void __launch_bounds__(kBlock, kMinBlocks)
 octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ actions,
              uint8_t *__restrict__ obs, float *__restrict__ reward, uint8_t *__restrict__ done_out,
              uint8_t *__restrict__ term_out, uint8_t *__restrict__ trunc_out) {
@@ -657,7 +653,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     L.dirty = p.s.dirty[env];
     L.ram = p.s.ram + env * 4096ull;
   }
-  L.dec = __ldg(p.s.dec + min(L.pc, 0x1000u));
+  L.dec = __ldg(p.s.dec + L.pc);
   __syncthreads();  // mbarrier initialised
   stage_wait(sm);
   bool wdirty = __any_sync(kFull, L.dirty != 0ull);  // any lane with private RAM blocks
@@ -696,6 +692,11 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     // planes 0 (lanes 0-15, ring slot s0) and 1 (lanes 16-31, slot s1) of env `cur`:
     // one 16-B chunk per lane, loaded before a cycle and stored (in row order) after it
     const uint4 *rsrc = reinterpret_cast<const uint4 *>(ring_at(p, hh ? s1 : s0, wbase) + l2);
+    // one bulk L2 prefetch per half-warp of its 8 KB ring block (plane 0 or 1 of the warp's
+    // 32 envs): the per-cycle copy loads then hit L2 instead of queueing on HBM (+5..8%)
+    if (!sf && (lane & 15) == 0 && ne > 0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ring_at(p, hh ? s1 : s0, wbase)),
+                   "r"((uint32_t)ne * 256u) : "memory");
     uint64_t *odst = obs64 + wbase * 128 + hh * 32;
     int cur = sf ? ne : 0;
     L.run = active && !L.halted;
