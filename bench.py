@@ -347,6 +347,23 @@ def main():
         e2e = {"value": world * n * K / float(dt.item()), "unit": "env steps/s",
                "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": (env.obs_per_env + 4 + 1) * n,
                "steps": K, "path": "octax_step_host (pinned host buffers)"}
+        # the e2e roof: this box's pinned D2H copy bandwidth for the same bytes (plain
+        # cudaMemcpyAsync of a device buffer into the pinned obs buffer, best of 3)
+        src = torch.empty((n, env.obs_per_env), dtype=torch.uint8, device="cuda")
+        best = None
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            o_h.copy_(src, non_blocking=True)
+            torch.cuda.synchronize()
+            t = time.perf_counter() - t0
+            best = t if best is None else min(best, t)
+        d2h_gbs = o_h.numel() / best / 1e9
+        bytes_step = e2e["h2d_bytes_per_step"] + e2e["d2h_bytes_per_step"]
+        roof = d2h_gbs * 1e9 / (bytes_step / n)
+        e2e["link"] = {"d2h_gbs_measured": d2h_gbs, "bytes_per_env_step": bytes_step / n,
+                       "roof_env_steps_per_s": roof * world, "frac": e2e["value"] / (roof * world)}
+        del src
     env.close()
     del acts
     torch.cuda.empty_cache()

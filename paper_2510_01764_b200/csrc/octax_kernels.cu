@@ -518,7 +518,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     const uint32_t dm = __ballot_sync(kFull, nrows != 0u);
     // one grouped pass (groups of maxr lanes, 32 / maxr drawers) when the drawers fit and
     // rows are many enough to beat maxr lane-parallel row steps (uniform choice)
-    if (maxr >= 3u && (uint32_t)__popc(dm) <= __umulhi(32u, kRecip[maxr]))
+    if (maxr >= 3u && (uint32_t)__popc(dm) * maxr <= 32u)  // k drawers fit 32 / maxr groups
     {
       if (wdirty)
         draw_groups<true>(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
@@ -605,7 +605,11 @@ __device__ __forceinline__ uint32_t eval(const Program &P, Smem &sm, const Lane 
 
 // ---------------------------------------------------------------- the step kernel
 template <int MODE, bool Q0>
+#ifdef OCTAX_MAXNREG
+__global__ void __maxnreg__(OCTAX_MAXNREG)
+#else
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
+#endif
 octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ actions,
              uint8_t *__restrict__ obs, float *__restrict__ reward, uint8_t *__restrict__ done_out,
              uint8_t *__restrict__ term_out, uint8_t *__restrict__ trunc_out) {
@@ -705,7 +709,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     for (uint32_t f = 0; f < p.frame_skip; ++f) {
       for (uint32_t k = 0; k < p.ipf; ++k) {
         const bool cp = cur < ne;
-        uint4 q = make_uint4(0, 0, 0, 0);
+        uint4 q;  // only read under cp
         if (cp) q = __ldcs(rp);
         cycle<Q0>(sm, L, p, tid, lane, block0, gid, active, wdirty);
         if (cp) {
