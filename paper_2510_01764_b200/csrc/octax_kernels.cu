@@ -151,6 +151,17 @@ __device__ __forceinline__ void put_rows(uint64_t *ob_env, uint32_t pl, uint32_t
   __stcs(ob_env + pl * 32u + (ra ^ 1u), ((uint64_t)q.w << 32) | q.z);
 }
 
+// Obs rows 2k, 2k+1 of env el from the shared framebuffer as ONE 16-B streaming store, for the
+// two-envs-per-pass loops (lanes 0-15 env el even, 16-31 env el odd: hh = el & 1).  Lane chunk
+// l2 = 2(lane & 15) covers positions l2, l2+1 = rows l2 ^ s, (l2+1) ^ s (s = el & 15); for odd
+// s that pair is reversed, so the lane reads positions l2 ^ hh, l2 ^ hh ^ 1 instead and writes
+// rows (l2 ^ s) & ~1 onwards in order.
+__device__ __forceinline__ void put_pair(const uint64_t *fb_env, uint64_t *ob_env, uint32_t pl, uint32_t l2,
+                                         uint32_t hh, uint32_t s) {
+  const uint64_t lo = fb_env[l2 ^ hh], hi = fb_env[l2 ^ hh ^ 1u];
+  __stcs(reinterpret_cast<ulonglong2 *>(ob_env + pl * 32u + ((l2 ^ s) & ~1u)), make_ulonglong2(lo, hi));
+}
+
 // ---------------------------------------------------------------- lane state
 struct Lane {
   uint32_t pc, sp, dt, st, halted, draw, episode;
@@ -678,8 +689,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       for (int e = 0; e < ne; e += 2)  // plane 2 <- step-start display, two envs per pass
         if (e + (int)hh < ne) {
           const uint32_t el = (uint32_t)(warp * 32 + e) + hh;
-          const uint4 q = *reinterpret_cast<const uint4 *>(&sm.fb[el * 32u + l2]);
-          put_rows(obs64 + (wbase + e + hh) * 128, 2u, l2 ^ (el & 15u), q);
+          put_pair(&sm.fb[el * 32u], obs64 + (wbase + e + hh) * 128, 2u, l2, hh, el & 15u);
         }
     } else {
       for (int e = 0; e < ne; ++e) {
@@ -808,14 +818,14 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   if (obs64) {
     for (int e = 0; e < ne; e += 2)
       if (e + (int)hh < ne) {
-        const uint32_t el = (uint32_t)(warp * 32 + e) + hh, ra = l2 ^ (el & 15u);
-        const uint4 q = *reinterpret_cast<const uint4 *>(&sm.fb[el * 32u + l2]);
+        const uint32_t el = (uint32_t)(warp * 32 + e) + hh, sw = el & 15u;
+        const uint64_t *fe = &sm.fb[el * 32u];
         uint64_t *ob = obs64 + (wbase + e + hh) * 128;
-        put_rows(ob, 3u, ra, q);
+        put_pair(fe, ob, 3u, l2, hh, sw);
         if (MODE != MODE_STEP || ((reset_mask >> (e + hh)) & 1u)) {
-          put_rows(ob, 0u, ra, q);
-          put_rows(ob, 1u, ra, q);
-          put_rows(ob, 2u, ra, q);
+          put_pair(fe, ob, 0u, l2, hh, sw);
+          put_pair(fe, ob, 1u, l2, hh, sw);
+          put_pair(fe, ob, 2u, l2, hh, sw);
         }
       }
   }
