@@ -349,7 +349,12 @@ __device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepP
   const uint32_t warp = (uint32_t)tid >> 5, wl = (uint32_t)tid & ~31u;
   const bool mine = ((dm >> lane) & 1u) != 0u;
   const uint32_t rank = (uint32_t)__popc(dm & ((1u << lane) - 1u));
+#ifdef OCTAX_V_PUB
+  // unconditional (no branch): non-drawers write slot 31, never read (<= 10 drawers here)
+  sm.dprm[warp][mine ? rank : 31u] = x0 | (y0 << 6) | (base << 11) | (nrows << 23) | ((uint32_t)lane << 27);
+#else
   if (mine) sm.dprm[warp][rank] = x0 | (y0 << 6) | (base << 11) | (nrows << 23) | ((uint32_t)lane << 27);
+#endif
   __syncwarp();
   // group g = lane / m, row r = lane % m (m = the warp's largest row count, 3..15)
   const uint32_t g = __umulhi((uint32_t)lane, kRecip[m]), r = (uint32_t)lane - g * m;
@@ -464,7 +469,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   nvx = HAS(d, D_VSALU) ? r8 : nvx;
   nvx = HAS(d, D_VSDT) ? L.dt : nvx;
   nvx = HAS(d, D_WAIT) ? L.kidx : nvx;
-  if (act && (d & L.wvm) != 0u) sm.V[ax] = (uint8_t)nvx;
+  sm.V[ax] = (uint8_t)((act && (d & L.wvm) != 0u) ? nvx : vx);  // unconditional: no branch around the ALU
   if (act && HAS(d, D_WVF)) VREG(15) = (uint8_t)f8;
   // ---- control flow and index / timer registers
   uint32_t npc = pc + 2u + skip2;
@@ -476,14 +481,12 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   I2 = HAS(d, D_INNN) ? nnn : I2;
   I2 = HAS(d, D_IADD) ? (I2 + vx) : I2;  // 16-bit I kept modulo 2^32: users mask (A18)
   I2 = HAS(d, D_IFONT) ? (0x50u + 5u * (vx & 15u)) : I2;
-  if (act) {
-    L.pc = npc;  // < 2^16: PC <= 0xFFE when active, stack entries are u16, BNNN masks
-    L.dec = __ldg(p.s.dec + L.pc);  // next cycle's word, in flight meanwhile
-    L.I = I2;
-    L.sp = nsp;
-    L.dt = HAS(d, D_DTW) ? vx : L.dt;
-    L.st = HAS(d, D_STW) ? vx : L.st;
-  }
+  L.pc = act ? npc : pc;  // < 2^16: PC <= 0xFFE when active, stack entries are u16, BNNN masks
+  L.dec = __ldg(p.s.dec + L.pc);  // next cycle's word, in flight meanwhile (re-read when idle)
+  L.I = act ? I2 : L.I;
+  L.sp = act ? nsp : L.sp;
+  L.dt = (act && HAS(d, D_DTW)) ? vx : L.dt;
+  L.st = (act && HAS(d, D_STW)) ? vx : L.st;
   const bool f33 = nn == 0x33u, f55 = nn == 0x55u;  // only meaningful under D_MEM
   // ---- vote-gated rare classes (one vote for CLS / CXNN / FX33-55-65 together)
   if (__any_sync(kFull, act && HAS(d, D_RARE))) {
