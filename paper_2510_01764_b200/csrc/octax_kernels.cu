@@ -349,12 +349,8 @@ __device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepP
   const uint32_t warp = (uint32_t)tid >> 5, wl = (uint32_t)tid & ~31u;
   const bool mine = ((dm >> lane) & 1u) != 0u;
   const uint32_t rank = (uint32_t)__popc(dm & ((1u << lane) - 1u));
-#ifdef OCTAX_V_PUB
   // unconditional (no branch): non-drawers write slot 31, never read (<= 10 drawers here)
   sm.dprm[warp][mine ? rank : 31u] = x0 | (y0 << 6) | (base << 11) | (nrows << 23) | ((uint32_t)lane << 27);
-#else
-  if (mine) sm.dprm[warp][rank] = x0 | (y0 << 6) | (base << 11) | (nrows << 23) | ((uint32_t)lane << 27);
-#endif
   __syncwarp();
   // group g = lane / m, row r = lane % m (m = the warp's largest row count, 3..15)
   const uint32_t g = __umulhi((uint32_t)lane, kRecip[m]), r = (uint32_t)lane - g * m;
