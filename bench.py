@@ -252,6 +252,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--envs", type=int, default=1 << 20, help="envs per GPU")
     ap.add_argument("--game", default="pong_standin")
+    ap.add_argument("--obs", default="packed", choices=["packed", "bool"],
+                    help="observation layout (bool = the paper's dense x-major [n,4,64,32])")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -280,7 +282,7 @@ def main():
         if world > 1:
             dist.barrier()
 
-    rom, spec = workloads.game(args.game)
+    rom, spec = workloads.game(args.game, obs_format=1 if args.obs == "bool" else 0)
     n = args.envs
     offset, _ = odist.shard(rank, world, n)
 
@@ -423,7 +425,7 @@ def main():
                                    "uniform random actions (device Philox generator), packed 4-plane obs",
                        "game": args.game, "envs_per_gpu": n, "global_envs": world * n,
                        "frame_skip": spec["frame_skip"], "instructions_per_frame": spec["instructions_per_frame"],
-                       "obs_format": "packed [n,4,32,8]", "parallelism": f"env-sharded x{world}",
+                       "obs_format": "packed [n,4,32,8]" if args.obs == "packed" else "bool [n,4,64,32] (x-major, P:146)", "parallelism": f"env-sharded x{world}",
                        "l2": f"inputs larger than L2: ~{ALG_BYTES_PER_ENV_STEP * n / 2**30:.2f} GiB "
                              "touched per step vs 126 MB L2 (no flush needed)"},
             "roofline": ({"bound": "alu", "achieved": alu["achieved"], "peak": alu["peak"], "unit": alu["unit"],
