@@ -488,7 +488,7 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
     if (pc <= 0xFFEu) {
       make_entry(((uint32_t)image[pc] << 8) | image[pc + 1], dtab, spec->quirks, dec[pc].x, dec[pc].y);
     } else {
-      dec[pc] = make_uint2(E_BAD, 0u);  // fetch past 0xFFE halts (A17)
+      dec[pc] = make_uint2(E_BAD, 1u << 18);  // fetch past 0xFFE halts (A17); SP delta 0
     }
   }
   ce = cudaMemcpyAsync(base + o_img, image, kStageBytes, cudaMemcpyHostToDevice, e->stream);

@@ -69,7 +69,9 @@ enum : uint32_t {
   A_SUB = 1u << 28, A_RSUB = 1u << 29, A_SHR = 1u << 30,                   // 8XY5, 8XY7, 8XY6
   A_SRCY = 1u << 31  // SHIFT_VY quirk: 8XY6 / 8XYE shift VY (never set for the modern profile)
 };
-constexpr uint32_t kDecEntries = 65536;  // every 16-bit PC: entries past 0xFFE halt (A17), so no clamp
+// every 16-bit PC (entries past 0xFFE halt, A17, so no clamp), plus a second 64K of E_BAD
+// entries fetched by lanes that are halted on entry or past n (PC bit 16 set in the kernel)
+constexpr uint32_t kDecEntries = 131072;
 #ifdef __CUDACC__
 __host__ __device__
 #endif

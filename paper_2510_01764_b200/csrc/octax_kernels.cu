@@ -169,7 +169,7 @@ struct Lane {
   uint32_t I;       // index register; only its low 16 bits are meaningful (FX1E wraps, A18)
   uint32_t keys;    // held key mask, 16 bits replicated into both halves
   uint32_t wvm;     // descriptor bits that write VX this step: D_WVX, + D_WAIT if a key is held
-  uint32_t stay;    // D_WAIT if no key is held (FX0A re-executes), else 0
+  uint32_t stay;    // entry bits that keep the PC: D_WAIT if no key is held (FX0A re-executes), E_BAD
   uint32_t kidx;    // lowest held key (FX0A result)
   uint64_t dirty;   // copy-on-write mask: block b (64 B) of RAM lives in HBM
   uint8_t *ram;
@@ -189,7 +189,7 @@ __device__ __forceinline__ uint32_t vbase(int tid) {
 __device__ __forceinline__ void set_keys(Lane &L, uint32_t km) {
   L.keys = km * 0x10001u;
   L.wvm = km ? (D_WVX | D_WAIT) : D_WVX;
-  L.stay = km ? 0u : D_WAIT;
+  L.stay = (km ? 0u : D_WAIT) | E_BAD;  // E_BAD: a faulting entry keeps its PC (cycle<Q0, false>)
   L.kidx = (uint32_t)(__ffs(km) - 1);
 }
 // Flag test written with a two-bit mask (kPad is never set in an entry): keeps the
@@ -403,11 +403,16 @@ __device__ __forceinline__ void draw_one(Smem &sm, const Lane &L, int tid, bool 
   if (vfw) VREG(15) = (uint8_t)hit;
 }
 
-template <bool Q0>
+// RF = true (startup segments): lanes run under the loop-carried flag L.run (= part && !halted).
+// RF = false (the step's frame loop): every lane runs the cycle; a lane that is halted, or
+// that halts, re-executes its faulting entry with no effect -- an invalid word's entry has no
+// effect flags and stays at its PC (E_BAD is in L.stay), a stack fault keeps PC and SP -- so
+// no run flag gates the core; L.run then only records "did not fault" for the timer tick.
+template <bool Q0, bool RF>
 __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, int tid, int lane, uint64_t block0,
                                       uint32_t gid, bool part, bool &wdirty) {
   const uint32_t quirks = Q0 ? 0u : p.quirks;  // Q0: modern profile specialisation
-  bool act = L.run;  // = part && !halted, maintained by the cycle loops
+  bool act = RF ? L.run : true;
   const uint32_t pc = L.pc;
   // ---- fetch + decode: the predecoded word at PC (L1-resident table, loaded at the end
   //      of the previous cycle; PCs past 0xFFE halt through the table).  Slow path: PC in
@@ -424,8 +429,14 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   const uint32_t nsp = L.sp + ((e.y >> 18) & 3u) - 1u;  // SP after 2NNN / 00EE
   // ---- faults halt the lane (A17, A20): invalid word / PC past 0xFFE, stack over/underflow
   const bool bad = HAS(d, E_BAD) || nsp > 16u;
-  act = act && !bad;
-  L.run = act;
+  if (RF) {
+    act = act && !bad;
+    L.run = act;
+  } else {
+    act = nsp <= 16u;  // gates PC / SP / stack only; an E_BAD entry carries no effect flags
+    L.run = !bad;
+  }
+  const bool ex = RF ? act : true;  // gate of the flag-driven effects
   // V[k] of this lane lives at vbase | voff(k) (VREG); kx = V[x], or V0 for BNNN
   const uint32_t vb = vbase(tid), ax = (e.y & 0x1FFu) | vb, vx = sm.V[ax], vy = sm.V[((e.y >> 9) & 0x1FFu) | vb];
   OCTAX_CHECK(ax < 16u * kBlock && (((e.y >> 9) & 0x1FFu) | vb) < 16u * kBlock);
@@ -465,30 +476,30 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   nvx = HAS(d, D_VSALU) ? r8 : nvx;
   nvx = HAS(d, D_VSDT) ? L.dt : nvx;
   nvx = HAS(d, D_WAIT) ? L.kidx : nvx;
-  sm.V[ax] = (uint8_t)((act && (d & L.wvm) != 0u) ? nvx : vx);  // unconditional: no branch around the ALU
-  if (act && HAS(d, D_WVF)) VREG(15) = (uint8_t)f8;
+  sm.V[ax] = (uint8_t)((ex && (d & L.wvm) != 0u) ? nvx : vx);  // unconditional: no branch around the ALU
+  if (ex && HAS(d, D_WVF)) VREG(15) = (uint8_t)f8;
   // ---- control flow and index / timer registers
   uint32_t npc = pc + 2u + skip2;
   npc = HAS(d, D_PCJ) ? nnn : npc;  // 1NNN, 2NNN
   npc = is_ret ? ret_pc : npc;
-  npc = (d & L.stay) != 0u ? pc : npc;  // A16: FX0A re-executes while no key
+  npc = (d & L.stay) != 0u ? pc : npc;  // A16: FX0A re-executes while no key; E_BAD stays
   npc = HAS(d, D_BJMP) ? ((nnn + vx) & 0xFFFu) : npc;  // vx = V0 or V[x] (JUMP_VX quirk)
   uint32_t I2 = L.I;
   I2 = HAS(d, D_INNN) ? nnn : I2;
   I2 = HAS(d, D_IADD) ? (I2 + vx) : I2;  // 16-bit I kept modulo 2^32: users mask (A18)
   I2 = HAS(d, D_IFONT) ? (0x50u + 5u * (vx & 15u)) : I2;
-  L.pc = act ? npc : pc;  // < 2^16: PC <= 0xFFE when active, stack entries are u16, BNNN masks
+  L.pc = act ? npc : pc;  // PC <= 0xFFE when running; halted-at-entry lanes carry bit 16 (see kDecEntries)
   L.dec = __ldg(p.s.dec + L.pc);  // next cycle's word, in flight meanwhile (re-read when idle)
-  L.I = act ? I2 : L.I;
+  L.I = ex ? I2 : L.I;
   L.sp = act ? nsp : L.sp;
-  L.dt = (act && HAS(d, D_DTW)) ? vx : L.dt;
-  L.st = (act && HAS(d, D_STW)) ? vx : L.st;
+  L.dt = (ex && HAS(d, D_DTW)) ? vx : L.dt;
+  L.st = (ex && HAS(d, D_STW)) ? vx : L.st;
   const bool f33 = nn == 0x33u, f55 = nn == 0x55u;  // only meaningful under D_MEM
   // ---- vote-gated rare classes (one vote for CLS / CXNN / FX33-55-65 together)
-  if (__any_sync(kFull, act && HAS(d, D_RARE))) {
-  const bool do_cls = act && HAS(d, E_CLS);
-  const bool do_rnd = act && HAS(d, D_RND);
-  const bool do_mem = act && HAS(d, D_MEM);
+  if (__any_sync(kFull, ex && HAS(d, D_RARE))) {
+  const bool do_cls = ex && HAS(d, E_CLS);
+  const bool do_rnd = ex && HAS(d, D_RND);
+  const bool do_mem = ex && HAS(d, D_MEM);
   if (__any_sync(kFull, do_cls)) {
     if (do_cls) {
 #pragma unroll
@@ -520,7 +531,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     wdirty = __any_sync(kFull, L.dirty != 0ull);
   }
   }
-  const bool do_draw = act && HAS(d, D_DRAW);
+  const bool do_draw = ex && HAS(d, D_DRAW);
   if (__any_sync(kFull, do_draw)) {
     const uint32_t y0 = vy & 31u;
     const uint32_t nrows = do_draw ? (((quirks & 8u) != 0u) ? n : min(n, 32u - y0)) : 0u;
@@ -552,7 +563,7 @@ __device__ __forceinline__ void run_frames(Smem &sm, Lane &L, const StepParams &
                                            uint32_t gid, bool part, uint32_t frames, bool &wdirty) {
   L.run = part && !L.halted;
   for (uint32_t f = 0; f < frames; ++f) {
-    for (uint32_t k = 0; k < p.ipf; ++k) cycle<Q0>(sm, L, p, tid, lane, block0, gid, part, wdirty);
+    for (uint32_t k = 0; k < p.ipf; ++k) cycle<Q0, true>(sm, L, p, tid, lane, block0, gid, part, wdirty);
     if (L.run) {
       L.dt -= (L.dt != 0u);
       L.st -= (L.st != 0u);
@@ -643,7 +654,9 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   if (tid == 0) stage_issue(sm, p.s.image, MODE == MODE_STEP ? ring_at(p, s2, block0) : nullptr);
 
   Lane L;
-  L.pc = 0x200; L.I = 0; L.sp = 0; L.dt = 0; L.st = 0; L.halted = 1; L.draw = 0; L.episode = 0;
+  // lanes past n and lanes halted on entry fetch from the E_BAD half of the decode table
+  // (PC bit 16), so the step's frame loop runs them without effect (cycle<Q0, false>)
+  L.pc = 0x10000u; L.I = 0; L.sp = 0; L.dt = 0; L.st = 0; L.halted = 1; L.draw = 0; L.episode = 0;
   set_keys(L, 0u);
   L.dirty = 0; L.ram = p.s.ram; L.stk_dirty = 0;
   uint32_t steps = 0, prev = 0;
@@ -657,6 +670,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     uint4 c = p.s.ctrl[env];
     L.pc = c.x & 0xFFFFu; L.I = c.x >> 16;
     L.sp = c.y & 255u; L.dt = (c.y >> 8) & 255u; L.st = (c.y >> 16) & 255u; L.halted = c.y >> 24;
+    if (L.halted) L.pc |= 0x10000u;
     L.draw = c.z; L.episode = c.w;
     uint4 b = p.s.book[env];
     steps = b.x; prev = b.y; ep_ret = (int32_t)b.z;
@@ -720,7 +734,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
         const bool cp = cur < ne;
         uint4 q;  // only read under cp
         if (cp) q = __ldcs(rp);
-        cycle<Q0>(sm, L, p, tid, lane, block0, gid, active, wdirty);
+        cycle<Q0, false>(sm, L, p, tid, lane, block0, gid, active, wdirty);
         if (cp) {
           put_rows(opl, 0u, l2 ^ ((uint32_t)cur & 15u), q);
           ++cur;
@@ -846,7 +860,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
 #pragma unroll
     for (int j = 0; j < 4; ++j) w[j] = *reinterpret_cast<const uint32_t *>(&sm.V[vbase(tid) | (j << 7)]);
     p.s.regs[env] = make_uint4(w[0], w[1], w[2], w[3]);
-    p.s.ctrl[env] = make_uint4(L.pc | (L.I << 16), L.sp | (L.dt << 8) | (L.st << 16) | (L.halted << 24),
+    p.s.ctrl[env] = make_uint4((L.pc & 0xFFFFu) | (L.I << 16), L.sp | (L.dt << 8) | (L.st << 16) | (L.halted << 24),
                                L.draw, L.episode);
     p.s.book[env] = make_uint4(steps, prev, (uint32_t)ep_ret, 0u);
     if (L.stk_dirty) {
