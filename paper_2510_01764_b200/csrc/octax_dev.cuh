@@ -135,7 +135,7 @@ struct DevState {
   uint64_t *ring;    // [4][n_pad][32] display history, slot-major (n_pad = n rounded up to
                      // kBlock, so a CTA's 128 envs are one contiguous 32 KB block per slot);
                      // u64 = one row in packed byte order; position j of env e holds row
-                     // j ^ (e & 15) -- the shared-memory framebuffer's swizzle, so ring <->
+                     // j ^ (e & 14) -- the shared-memory framebuffer's swizzle (kSwz), so ring <->
                      // smem moves are plain TMA bulk copies
   uint64_t ring_stride;  // u64 per ring slot = n_pad * 32
   unsigned long long *stats;  // [4] {returns, episodes, steps, err}

@@ -55,6 +55,14 @@ __constant__ uint32_t kRecip[16] = {0u, 0u, 0x80000000u, 0x55555556u, 0x40000000
                                     0x2AAAAAABu, 0x24924925u, 0x20000000u, 0x1C71C71Du, 0x1999999Au,
                                     0x1745D175u, 0x15555556u, 0x13B13B14u, 0x12492493u, 0x11111112u};
 
+// framebuffer / ring row swizzle: row r of env e sits at position r ^ (e & kSwz).  14 keeps row
+// pairs (2k, 2k+1) in order inside every 16-B chunk, so obs rows move as 16-B stores; 8 envs
+// (not 16) then differ in the position of a given row (A/B: +0.1..0.6% over 15).
+#ifndef OCTAX_SWZ
+#define OCTAX_SWZ 14
+#endif
+constexpr uint32_t kSwz = OCTAX_SWZ;
+
 struct __align__(128) Smem {
   uint8_t img[kImageBytes];                  // pristine image (TMA destination) ...
   uint32_t dtab[kDescEntries];               // ... immediately followed by the decode table
@@ -72,7 +80,7 @@ size_t smem_bytes() { return sizeof(Smem); }
 // framebuffer row `r` of CTA-local env `e`: XOR swizzle on the low 4 row bits
 __device__ __forceinline__ uint32_t fb_idx(uint32_t e, uint32_t r) {
   OCTAX_CHECK(e < (uint32_t)kBlock && r < 32u);
-  return e * 32u + (r ^ (e & 15u));
+  return e * 32u + (r ^ (e & kSwz));
 }
 
 __device__ __forceinline__ uint64_t bswap64(uint64_t v) {
@@ -138,26 +146,31 @@ __device__ __forceinline__ void fb_store_issue(const Smem &sm, uint64_t *dst) {
                : "memory");
 }
 
-// ring slot `slot` of handle-local env `e` (32 positions; position j holds row j ^ (e & 15))
+// ring slot `slot` of handle-local env `e` (32 positions; position j holds row j ^ (e & kSwz))
 __device__ __forceinline__ uint64_t *ring_at(const StepParams &p, uint32_t slot, uint64_t e) {
   OCTAX_CHECK(slot < 4u && e * 32u < p.s.ring_stride);
   return p.s.ring + (uint64_t)slot * p.s.ring_stride + e * 32u;
 }
 
-// obs plane `pl` of a pair of envs from 16-B chunks in position order: lanes 0-15 serve
-// env e, 16-31 env e+1; chunk 2l..2l+1 holds rows ra, ra^1 with ra = 2l ^ (e & 15).
+// obs plane `pl` of an env from one lane's 16-B chunk of positions 2l, 2l+1 = rows ra, ra^1
+// with ra = 2l ^ (e & kSwz); with the even swizzle ra is even, so the chunk is one 16-B store.
 __device__ __forceinline__ void put_rows(uint64_t *ob_env, uint32_t pl, uint32_t ra, uint4 q) {
-  __stcs(ob_env + pl * 32u + ra, ((uint64_t)q.y << 32) | q.x);
-  __stcs(ob_env + pl * 32u + (ra ^ 1u), ((uint64_t)q.w << 32) | q.z);
+  if ((kSwz & 1u) == 0u) {  // even swizzle: ra is even, the chunk is rows ra, ra+1 in order
+    __stcs(reinterpret_cast<uint4 *>(ob_env + pl * 32u + ra), q);
+  } else {
+    __stcs(ob_env + pl * 32u + ra, ((uint64_t)q.y << 32) | q.x);
+    __stcs(ob_env + pl * 32u + (ra ^ 1u), ((uint64_t)q.w << 32) | q.z);
+  }
 }
 
 // Obs rows 2k, 2k+1 of env el from the shared framebuffer as ONE 16-B streaming store, for the
 // two-envs-per-pass loops (lanes 0-15 env el even, 16-31 env el odd: hh = el & 1).  Lane chunk
-// l2 = 2(lane & 15) covers positions l2, l2+1 = rows l2 ^ s, (l2+1) ^ s (s = el & 15); for odd
-// s that pair is reversed, so the lane reads positions l2 ^ hh, l2 ^ hh ^ 1 instead and writes
-// rows (l2 ^ s) & ~1 onwards in order.
+// l2 = 2(lane & 15) covers positions l2, l2+1 = rows l2 ^ s, (l2+1) ^ s (s = el & kSwz); for an
+// odd s (OCTAX_SWZ=15) that pair is reversed, so the lane reads positions l2 ^ (s & 1),
+// l2 ^ (s & 1) ^ 1 instead and writes rows (l2 ^ s) & ~1 onwards in order.
 __device__ __forceinline__ void put_pair(const uint64_t *fb_env, uint64_t *ob_env, uint32_t pl, uint32_t l2,
-                                         uint32_t hh, uint32_t s) {
+                                         uint32_t s) {
+  const uint32_t hh = s & 1u;
   const uint64_t lo = fb_env[l2 ^ hh], hi = fb_env[l2 ^ hh ^ 1u];
   __stcs(reinterpret_cast<ulonglong2 *>(ob_env + pl * 32u + ((l2 ^ s) & ~1u)), make_ulonglong2(lo, hi));
 }
@@ -302,7 +315,7 @@ __device__ __forceinline__ void draw_lanes(Smem &sm, Lane &L, const StepParams &
   const bool wrap = (quirks & 8u) != 0;
   bool slowb = do_draw & (base + 15u > 0xFFFu);
   if (wdirty) slowb |= do_draw & (((L.dirty >> (base >> 6)) & 3ull) != 0ull);
-  const uint32_t sh = x0 & 7u, q8 = (x0 >> 3) * 8u, swz = (uint32_t)tid & 15u;
+  const uint32_t sh = x0 & 7u, q8 = (x0 >> 3) * 8u, swz = (uint32_t)tid & kSwz;
   uint64_t *rows = &sm.fb[(uint32_t)tid * 32u];
   uint64_t hit = 0;
   if (!wrap && !__any_sync(kFull, slowb)) {
@@ -373,7 +386,7 @@ __device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepP
     const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> (ox & 7u), 0, 0x4401);
     const uint64_t mk = wrap ? ((w << q8) | (q8 ? (w >> (64u - q8)) : 0ull)) : (w << q8);
     OCTAX_CHECK(oe < (uint32_t)kBlock && yy < 32u);
-    uint64_t *row = &sm.fb[oe * 32u + (yy ^ (oe & 15u))];
+    uint64_t *row = &sm.fb[oe * 32u + (yy ^ (oe & kSwz))];
     const uint64_t old = *row;
     *row = old ^ mk;
     hit = (old & mk) != 0ull;
@@ -395,7 +408,7 @@ __device__ __forceinline__ void draw_one(Smem &sm, const Lane &L, int tid, bool 
     const uint32_t q8 = x0 & 0x38u;
     const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> (x0 & 7u), 0, 0x4401);
     const uint64_t mk = (quirks & 8u) ? ((w << q8) | (q8 ? (w >> (64u - q8)) : 0ull)) : (w << q8);
-    uint64_t *row = &sm.fb[(uint32_t)tid * 32u + (y0 ^ ((uint32_t)tid & 15u))];
+    uint64_t *row = &sm.fb[(uint32_t)tid * 32u + (y0 ^ ((uint32_t)tid & kSwz))];
     const uint64_t old = *row;
     *row = old ^ mk;
     hit = (old & mk) != 0ull;
@@ -702,7 +715,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       for (int e = 0; e < ne; e += 2)  // plane 2 <- step-start display, two envs per pass
         if (e + (int)hh < ne) {
           const uint32_t el = (uint32_t)(warp * 32 + e) + hh;
-          put_pair(&sm.fb[el * 32u], obs64 + (wbase + e + hh) * 128, 2u, l2, hh, el & 15u);
+          put_pair(&sm.fb[el * 32u], obs64 + (wbase + e + hh) * 128, 2u, l2, el & kSwz);
         }
     } else {
       for (int e = 0; e < ne; ++e) {
@@ -736,7 +749,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
         if (cp) q = __ldcs(rp);
         cycle<Q0, false>(sm, L, p, tid, lane, block0, gid, active, wdirty);
         if (cp) {
-          put_rows(opl, 0u, l2 ^ ((uint32_t)cur & 15u), q);
+          put_rows(opl, 0u, l2 ^ ((uint32_t)cur & kSwz), q);
           ++cur;
           rp += 16;
           opl += 128;
@@ -754,7 +767,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       }
     }
 #pragma unroll 4
-    for (int e = cur; e < ne; ++e) put_rows(odst + e * 128, 0u, l2 ^ ((uint32_t)e & 15u), __ldcs(rsrc + e * 16));
+    for (int e = cur; e < ne; ++e) put_rows(odst + e * 128, 0u, l2 ^ ((uint32_t)e & kSwz), __ldcs(rsrc + e * 16));
     if (active) L.halted = !L.run;
     if (active) {
       const uint32_t s = eval(p.score, sm, L, tid);
@@ -831,14 +844,14 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   if (obs64) {
     for (int e = 0; e < ne; e += 2)
       if (e + (int)hh < ne) {
-        const uint32_t el = (uint32_t)(warp * 32 + e) + hh, sw = el & 15u;
+        const uint32_t el = (uint32_t)(warp * 32 + e) + hh, sw = el & kSwz;
         const uint64_t *fe = &sm.fb[el * 32u];
         uint64_t *ob = obs64 + (wbase + e + hh) * 128;
-        put_pair(fe, ob, 3u, l2, hh, sw);
+        put_pair(fe, ob, 3u, l2, sw);
         if (MODE != MODE_STEP || ((reset_mask >> (e + hh)) & 1u)) {
-          put_pair(fe, ob, 0u, l2, hh, sw);
-          put_pair(fe, ob, 1u, l2, hh, sw);
-          put_pair(fe, ob, 2u, l2, hh, sw);
+          put_pair(fe, ob, 0u, l2, sw);
+          put_pair(fe, ob, 1u, l2, sw);
+          put_pair(fe, ob, 2u, l2, sw);
         }
       }
   }
@@ -976,9 +989,9 @@ __global__ void get_states_kernel(StepParams p, const uint64_t *__restrict__ ids
       for (int q = 0; q < 4; ++q) c[56 + 4 * k + q] = (uint8_t)(f[k] >> (8 * q));
   }
   // display (slot h) and history planes 0..2 = slots h-3, h-2, h-1
-  // canonical byte i = row i>>3, byte i&7; the ring holds row r at position r ^ (env & 15)
+  // canonical byte i = row i>>3, byte i&7; the ring holds row r at position r ^ (env & kSwz)
   for (int i = t; i < 256; i += blockDim.x) {
-    const uint32_t j = (((uint32_t)i >> 3) ^ (uint32_t)(env & 15u)) * 8u + ((uint32_t)i & 7u);
+    const uint32_t j = (((uint32_t)i >> 3) ^ (uint32_t)(env & kSwz)) * 8u + ((uint32_t)i & 7u);
     c[80 + i] = reinterpret_cast<const uint8_t *>(ring_at(p, h & 3, env))[j];
     c[336 + i] = reinterpret_cast<const uint8_t *>(ring_at(p, (h + 1) & 3, env))[j];
     c[592 + i] = reinterpret_cast<const uint8_t *>(ring_at(p, (h + 2) & 3, env))[j];
@@ -1007,7 +1020,7 @@ __global__ void set_state_kernel(StepParams p, uint64_t env, const uint8_t *__re
     p.s.dirty[env] = ~0ull;  // whole RAM materialised from the canonical bytes
   }
   for (int i = t; i < 256; i += blockDim.x) {
-    const uint32_t j = (((uint32_t)i >> 3) ^ (uint32_t)(env & 15u)) * 8u + ((uint32_t)i & 7u);
+    const uint32_t j = (((uint32_t)i >> 3) ^ (uint32_t)(env & kSwz)) * 8u + ((uint32_t)i & 7u);
     reinterpret_cast<uint8_t *>(ring_at(p, h & 3, env))[j] = c[80 + i];
     reinterpret_cast<uint8_t *>(ring_at(p, (h + 1) & 3, env))[j] = c[336 + i];
     reinterpret_cast<uint8_t *>(ring_at(p, (h + 2) & 3, env))[j] = c[592 + i];
