@@ -747,6 +747,10 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
         const bool cp = cur < ne;
         uint4 q;  // only read under cp
         if (cp) q = __ldcs(rp);
+        // L1 prefetch of the chunk two cycles ahead (from the L2-resident ring block): its load
+        // is then an L1 hit, and the store at the end of that cycle does not wait on L2 (A/B:
+        // +3% pong, +6..7% brix / Target Shooter; one or three cycles ahead are slower)
+        if (cur + 2 < ne) asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + 32));
         cycle<Q0, false>(sm, L, p, tid, lane, block0, gid, active, wdirty);
         if (cp) {
           put_rows(opl, 0u, l2 ^ ((uint32_t)cur & kSwz), q);
