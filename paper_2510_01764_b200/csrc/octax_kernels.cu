@@ -450,6 +450,10 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     L.run = !bad;
   }
   const bool ex = RF ? act : true;  // gate of the flag-driven effects
+  // warp votes for the gated classes, taken as soon as the entry is known so the branches at
+  // the end of the core do not wait on them (A/B +1%)
+  const bool any_rare = __any_sync(kFull, ex && HAS(d, D_RARE));
+  const bool any_draw = __any_sync(kFull, ex && HAS(d, D_DRAW));
   // V[k] of this lane lives at vbase | voff(k) (VREG); kx = V[x], or V0 for BNNN
   const uint32_t vb = vbase(tid), ax = (e.y & 0x1FFu) | vb, vx = sm.V[ax], vy = sm.V[((e.y >> 9) & 0x1FFu) | vb];
   OCTAX_CHECK(ax < 16u * kBlock && (((e.y >> 9) & 0x1FFu) | vb) < 16u * kBlock);
@@ -509,7 +513,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   L.st = (ex && HAS(d, D_STW)) ? vx : L.st;
   const bool f33 = nn == 0x33u, f55 = nn == 0x55u;  // only meaningful under D_MEM
   // ---- vote-gated rare classes (one vote for CLS / CXNN / FX33-55-65 together)
-  if (__any_sync(kFull, ex && HAS(d, D_RARE))) {
+  if (any_rare) {
   const bool do_cls = ex && HAS(d, E_CLS);
   const bool do_rnd = ex && HAS(d, D_RND);
   const bool do_mem = ex && HAS(d, D_MEM);
@@ -545,7 +549,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   }
   }
   const bool do_draw = ex && HAS(d, D_DRAW);
-  if (__any_sync(kFull, do_draw)) {
+  if (any_draw) {
     const uint32_t y0 = vy & 31u;
     const uint32_t nrows = do_draw ? (((quirks & 8u) != 0u) ? n : min(n, 32u - y0)) : 0u;
     const uint32_t maxr = __reduce_max_sync(kFull, nrows);
