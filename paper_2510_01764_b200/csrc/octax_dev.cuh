@@ -13,7 +13,6 @@ namespace octax {
 #endif
 constexpr int kBlock = OCTAX_BLOCK;  // envs (threads) per CTA (a multiple of 32)
 constexpr int kMinBlocks = OCTAX_MINB;  // resident CTAs per SM the step kernel is built for
-constexpr int kFbStride = 33;        // u64 per env row block in smem (32 rows + 1 pad)
 constexpr int kMaxStartup = 32;
 constexpr int kMaxOps = 64;
 constexpr int kMaxDepth = 8;

@@ -643,7 +643,7 @@ __device__ __forceinline__ uint32_t eval(const Program &P, Smem &sm, const Lane 
 
 // ---------------------------------------------------------------- the step kernel
 template <int MODE, bool Q0>
-#ifdef OCTAX_MAXNREG
+#ifdef OCTAX_MAXNREG  // A/B knob for other CTA shapes (build.py --out ... -D OCTAX_MAXNREG=N)
 __global__ void __maxnreg__(OCTAX_MAXNREG)
 #else
 __global__ void __launch_bounds__(kBlock, kMinBlocks)
