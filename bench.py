@@ -330,6 +330,15 @@ def main():
                "ncu_alu_pipe_pct_of_peak": im.get("alu_pipe_pct_of_peak"),
                "sm_mhz": f_sm / 1e6, "source": im.get("source")}
 
+    # issue roof (SURVEY d.2): 148 SMs x 4 schedulers x 1 warp instruction per cycle x f_SM,
+    # against all warp instructions per env step measured by ncu (same source as the ALU count)
+    issue = None
+    if im and im.get("warp_instr_per_env_step"):
+        peak_iss = 148 * 4 * f_sm / 1e9
+        ach_iss = im["warp_instr_per_env_step"] * value / world / 1e9
+        issue = {"achieved": ach_iss, "peak": peak_iss, "unit": "G warp-instr/s", "frac": ach_iss / peak_iss,
+                 "warp_instr_per_env_step": im["warp_instr_per_env_step"]}
+
     # ---- e2e through the host-buffer C-ABI call (H2D actions, D2H obs/reward/done)
     e2e = None
     if not args.no_e2e:
@@ -430,7 +439,7 @@ def main():
                              "touched per step vs 126 MB L2 (no flush needed)"},
             "roofline": ({"bound": "alu", "achieved": alu["achieved"], "peak": alu["peak"], "unit": alu["unit"],
                           "frac": alu["frac"], "traffic": traffic, "kernel": "octax_kernel<MODE_STEP>",
-                          "kernel_ms_median": kernel_ms, "alu": alu,
+                          "kernel_ms_median": kernel_ms, "alu": alu, "issue": issue,
                           "hbm": {"achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                                   "alg_bytes_per_env_step": ALG_BYTES_PER_ENV_STEP, "peak_source": peak_src,
                                   "roof_env_steps_per_s": hbm_peak * 1e9 / ALG_BYTES_PER_ENV_STEP}}
