@@ -296,6 +296,15 @@ def main():
         env.stats_device(st)
         stream.synchronize()
         odist.reduce_stats(st)
+    # per-env 64-bit state digests after the timed steps (SURVEY d.1 item 4): rank 0's shard
+    # sum is the same for every N (trajectories are keyed by global id), the all-rank sum
+    # covers every env of the job (int64 all-reduce = sum mod 2^64)
+    _, dsum = env.state_digests()
+    dall = torch.tensor([dsum - (1 << 64) if dsum >= (1 << 63) else dsum], dtype=torch.int64, device="cuda")
+    odist.reduce_stats(dall)
+    digest = {"rank0_shard_sum": f"{dsum:016x}" if rank == 0 else None,
+              "all_ranks_sum": f"{int(dall.item()) % (1 << 64):016x}", "envs": world * n,
+              "def": "sum mod 2^64 of FNV-1a-64 of each env's canonical state (octax_state_digests)"}
     t_ms = odist.max_over_ranks(torch.tensor([total_ms], dtype=torch.float64, device="cuda"))
     t_max = float(t_ms.item())
     value = world * n * args.steps / (t_max / 1e3)
@@ -450,6 +459,7 @@ def main():
                           "peak_source": peak_src}),
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "state_digest": digest,
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "stats": [int(x) for x in st.cpu().tolist()],

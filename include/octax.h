@@ -190,6 +190,15 @@ octax_status octax_get_states(octax_env *e, const uint64_t *envs, uint64_t count
                               uint8_t *canon_out);
 octax_status octax_set_state(octax_env *e, uint64_t env, const uint8_t *canon_in);
 
+/* Per-env 64-bit state digests: FNV-1a 64 (offset 0xCBF29CE484222325, prime 0x100000001B3)
+ * over the 5,200 canonical bytes of octax_get_state, for local envs [first, first+count).
+ * digests_out: host uint64 [count] or NULL; sum_out: host, the sum of the digests mod 2^64,
+ * or NULL (not both NULL).  Because every trajectory is keyed by the global env id (A13), the
+ * digests of an env are identical for any sharding.
+ * Synchronises the stream; OCTAX_E_INVALID_ARG on a bad range. */
+octax_status octax_state_digests(octax_env *e, uint64_t first, uint64_t count, uint64_t *digests_out,
+                                 uint64_t *sum_out);
+
 /* Handle facts: n_envs, n_actions, obs bytes per env, device bytes allocated. */
 octax_status octax_info(octax_env *e, uint64_t out4[4]);
 

@@ -27,6 +27,8 @@ cudaError_t launch_expand_obs(uint64_t n, const uint8_t *packed, uint8_t *dense,
                               const uint8_t *row_mask = nullptr);
 cudaError_t launch_get_states(const StepParams &p, const uint64_t *ids, uint64_t count, uint8_t *out,
                               cudaStream_t stream);
+cudaError_t launch_state_digests(const StepParams &p, uint64_t first, uint64_t count, uint8_t *canon,
+                                 uint64_t *out, cudaStream_t stream);
 cudaError_t launch_set_state(const StepParams &p, uint64_t env, const uint8_t *canon, cudaStream_t stream);
 }  // namespace octax
 
@@ -637,6 +639,33 @@ extern "C" octax_status octax_get_states(octax_env *e, const uint64_t *envs, uin
   CU(cudaMemcpyAsync(canon_out, e->d_canon, (size_t)OCTAX_CANON_BYTES * count, cudaMemcpyDeviceToHost, e->stream),
      "D2H canon");
   CU(cudaStreamSynchronize(e->stream), "sync");
+  return OCTAX_OK;
+}
+
+extern "C" octax_status octax_state_digests(octax_env *e, uint64_t first, uint64_t count,
+                                            uint64_t *digests_out, uint64_t *sum_out) {
+  if (!e || (!digests_out && !sum_out)) return set_err(OCTAX_E_INVALID_ARG, "NULL argument");
+  if (first > e->n || count > e->n - first) return set_err(OCTAX_E_INVALID_ARG, "env range out of bounds");
+  DeviceGuard g(e->device);
+  const uint64_t chunk = count < 65536 ? count : 65536;
+  uint64_t sum = 0;
+  if (count) {
+    octax_status st = ensure_canon(e, chunk);
+    if (st != OCTAX_OK) return st;
+    std::vector<uint64_t> h(chunk);
+    for (uint64_t k = 0; k < count; k += chunk) {
+      const uint64_t m = count - k < chunk ? count - k : chunk;
+      // d_ids doubles as the digest buffer (8 B per env, chunk entries)
+      CU(launch_state_digests(e->p, first + k, m, e->d_canon, e->d_ids, e->stream), "digest kernels");
+      CU(cudaMemcpyAsync(h.data(), e->d_ids, 8 * m, cudaMemcpyDeviceToHost, e->stream), "D2H digests");
+      CU(cudaStreamSynchronize(e->stream), "sync");
+      for (uint64_t q = 0; q < m; ++q) {
+        if (digests_out) digests_out[k + q] = h[q];
+        sum += h[q];
+      }
+    }
+  }
+  if (sum_out) *sum_out = sum;
   return OCTAX_OK;
 }
 

@@ -974,8 +974,9 @@ __global__ void __launch_bounds__(256) expand_obs_kernel(uint64_t n, const uint8
 }
 
 // canonical per-env state (DESIGN.md layout), one CTA of 128 threads per requested env
-__global__ void get_states_kernel(StepParams p, const uint64_t *__restrict__ ids, uint8_t *__restrict__ out) {
-  const uint64_t env = ids[blockIdx.x];
+__global__ void get_states_kernel(StepParams p, const uint64_t *__restrict__ ids, uint64_t first,
+                                  uint8_t *__restrict__ out) {
+  const uint64_t env = ids ? ids[blockIdx.x] : first + blockIdx.x;  // ids == nullptr: a range
   uint8_t *c = out + (uint64_t)blockIdx.x * 5200;
   const int t = threadIdx.x;
   const uint32_t h = p.head;
@@ -1081,7 +1082,31 @@ cudaError_t launch_expand_obs(uint64_t n, const uint8_t *packed, uint8_t *dense,
 
 cudaError_t launch_get_states(const StepParams &p, const uint64_t *ids, uint64_t count, uint8_t *out,
                               cudaStream_t stream) {
-  get_states_kernel<<<(unsigned)count, 128, 0, stream>>>(p, ids, out);
+  get_states_kernel<<<(unsigned)count, 128, 0, stream>>>(p, ids, 0, out);
+  return cudaGetLastError();
+}
+
+// FNV-1a 64 over each env's 5,200 canonical bytes (octax_state_digests), one thread per env
+__global__ void digest_kernel(const uint8_t *__restrict__ canon, uint64_t count, uint64_t *__restrict__ out) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= count) return;
+  const uint4 *c = reinterpret_cast<const uint4 *>(canon + j * 5200);  // 5,200 = 325 x 16 B
+  uint64_t h = 0xCBF29CE484222325ull;
+  for (int k = 0; k < 325; ++k) {
+    const uint4 v = c[k];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) h = (h ^ ((w[q] >> (8 * b)) & 255u)) * 0x100000001B3ull;
+  }
+  out[j] = h;
+}
+
+cudaError_t launch_state_digests(const StepParams &p, uint64_t first, uint64_t count, uint8_t *canon,
+                                 uint64_t *out, cudaStream_t stream) {
+  get_states_kernel<<<(unsigned)count, 128, 0, stream>>>(p, nullptr, first, canon);
+  digest_kernel<<<(unsigned)((count + 127) / 128), 128, 0, stream>>>(canon, count, out);
   return cudaGetLastError();
 }
 

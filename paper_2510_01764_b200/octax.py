@@ -26,7 +26,7 @@ OBS_STACK_FRAMES = 16
 SYMBOLS = (
     "octax_create", "octax_reset", "octax_step", "octax_step_ex", "octax_step_host", "octax_gen_actions",
     "octax_stats", "octax_stats_device", "octax_get_state", "octax_get_states",
-    "octax_set_state", "octax_info", "octax_destroy", "octax_last_error",
+    "octax_set_state", "octax_state_digests", "octax_info", "octax_destroy", "octax_last_error",
 )
 
 
@@ -91,6 +91,7 @@ def load_library():
     L.octax_get_state.argtypes = [P, u64, P]
     L.octax_get_states.argtypes = [P, P, u64, P]
     L.octax_set_state.argtypes = [P, u64, P]
+    L.octax_state_digests.argtypes = [P, u64, u64, P, P]
     L.octax_info.argtypes = [P, P]
     L.octax_destroy.argtypes = [P]
     L.octax_destroy.restype = None
@@ -252,6 +253,16 @@ class OctaxEnv:
         c = np.ascontiguousarray(canon, dtype=np.uint8)
         assert c.shape == (CANON_BYTES,)
         _check(load_library().octax_set_state(self._h, env, ctypes.c_void_p(c.ctypes.data)))
+
+    def state_digests(self, first: int = 0, count: int | None = None):
+        """(digests uint64 [count], their sum mod 2^64) for local envs [first, first+count):
+        FNV-1a 64 over each env's canonical state bytes (include/octax.h)."""
+        n = self.n if count is None else count
+        out = np.zeros(n, np.uint64)
+        tot = np.zeros(1, np.uint64)
+        _check(load_library().octax_state_digests(self._h, first, n, ctypes.c_void_p(out.ctypes.data),
+                                                  ctypes.c_void_p(tot.ctypes.data)))
+        return out, int(tot[0])
 
     def info(self):
         out = np.zeros(4, np.uint64)

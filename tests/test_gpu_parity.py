@@ -305,6 +305,46 @@ def test_shard_invariance_r248_with_stats(world):
         agg += st
     fs, frc = full.stats()
     assert np.array_equal(agg, fs) and fs[1] > 0
+    # the per-env 64-bit state digests (SURVEY d.1 item 4) agree env by env across R
+    fd, fsum = full.state_digests()
+    psum = 0
+    for off, cnt, env in parts:
+        d, ps = env.state_digests()
+        assert np.array_equal(d, fd[off:off + cnt])
+        psum = (psum + ps) % 2**64
+    assert psum == fsum
+
+
+def _fnv1a64(b: bytes) -> int:
+    h = 0xCBF29CE484222325
+    for x in b:
+        h = ((h ^ x) * 0x100000001B3) % 2**64
+    return h
+
+
+def test_state_digests_definition():
+    """octax_state_digests = FNV-1a 64 of the canonical bytes (include/octax.h), written out
+    here independently, on sampled envs of a ragged handle after divergent steps; sub-ranges
+    and chunking (count > 65,536) agree with the full range; bad ranges are refused."""
+    rom, spec = workloads.game("brix_standin", max_episode_steps=30)
+    n = 70_001
+    g = _gpu_env(rom, spec, n, 3)
+    a = torch.empty(n, dtype=torch.int32, device="cuda")
+    for t in range(12):
+        g.gen_actions(5, t, a)
+        g.step(a)
+    d, tot = g.state_digests()
+    assert tot == int(d.astype(object).sum()) % 2**64
+    ids = [0, 1, 127, 128, 65535, 65536, n - 1]
+    canon = g.get_states(ids)
+    for j, c in zip(ids, canon):
+        assert int(d[j]) == _fnv1a64(bytes(c))
+    d2, _ = g.state_digests(65530, 20)
+    assert np.array_equal(d2, d[65530:65550])
+    assert len(np.unique(d)) > n // 2   # distinct states hash apart
+    from paper_2510_01764_b200.octax import OctaxError
+    with pytest.raises(OctaxError):
+        g.state_digests(n - 5, 10)
 
 
 def test_gen_actions_matches_oracle_generator():
