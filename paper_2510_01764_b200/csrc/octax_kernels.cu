@@ -32,6 +32,7 @@
 // the CPU oracle in oracle/.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cassert>
 #include <cstdint>
 
@@ -1043,12 +1044,17 @@ __global__ void set_state_kernel(StepParams p, uint64_t env, const uint8_t *__re
 template <int MODE, bool Q0>
 static cudaError_t launch_variant(const StepParams &p, const int32_t *actions, uint8_t *obs, float *reward,
                                   uint8_t *done, uint8_t *term, uint8_t *trunc, cudaStream_t stream) {
-  static bool attr_set = false;  // per template instance
+  // the dynamic-smem opt-in is per device and per kernel instance: one bit per device ordinal
+  static std::atomic<uint64_t> attr_set{0};
   const size_t smem = sizeof(Smem);
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(octax_kernel<MODE, Q0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_set.load(std::memory_order_relaxed) & bit)) {
+    e = cudaFuncSetAttribute(octax_kernel<MODE, Q0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.fetch_or(bit, std::memory_order_relaxed);
   }
   const unsigned grid = (unsigned)((p.n + kBlock - 1) / kBlock);
   octax_kernel<MODE, Q0><<<grid, kBlock, smem, stream>>>(p, actions, obs, reward, done, term, trunc);
