@@ -461,6 +461,8 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
          o_book = carve(16 * n), o_stack = carve(32 * n), o_dirty = carve(8 * n),
          o_ring = carve(1024 * ((n + kBlock - 1) / kBlock * kBlock)),
          o_ram = carve(4096 * n);
+  // deferred-reset list (only for specs with startup segments)
+  const size_t o_rcnt = spec->n_startup ? carve(4) : 0, o_rids = spec->n_startup ? carve(4 * n) : 0;
   e->block_bytes = off;
   cudaError_t ce = cudaMalloc(&e->block, off);
   if (ce != cudaSuccess) { free_env(e); return cuda_err(ce, "cudaMalloc(state)"); }
@@ -476,6 +478,8 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   p.s.ring = (uint64_t *)(base + o_ring);
   p.s.ring_stride = (n + kBlock - 1) / kBlock * kBlock * 32;
   p.s.ram = base + o_ram;
+  p.reset_count = spec->n_startup ? (uint32_t *)(base + o_rcnt) : nullptr;
+  p.reset_ids = spec->n_startup ? (uint32_t *)(base + o_rids) : nullptr;
   // state is fully written by the reset kernel; zero the small fields anyway
   ce = cudaMemsetAsync(base, 0, o_ring, e->stream);
   if (ce != cudaSuccess) { free_env(e); return cuda_err(ce, "cudaMemset"); }

@@ -148,6 +148,8 @@ struct StepParams {
   uint8_t *final_obs;      // packed [n][4][32][8]: obs of the terminal transition, done envs only
   int32_t *ep_ret_out;     // return of the episode that ended this step (0 if none)
   uint32_t *ep_len_out;    // its length in steps (0 if none)
+  uint32_t *reset_count;   // deferred resets (specs with startup segments): [1] counter and
+  uint32_t *reset_ids;     // [n] env ids appended by the step kernel, run by reset_kernel
   uint64_t n;
   uint64_t env_offset;
   uint64_t seed;

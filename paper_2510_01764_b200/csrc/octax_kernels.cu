@@ -248,6 +248,7 @@ __device__ __forceinline__ void power_on(Smem &sm, Lane &L, const StepParams &p,
 // with 4 ballots (counts are 4-bit), owners publish (lane, params) into a per-warp
 // smem map at their start item, and each item finds its owner as the highest
 // start bit at or below it (one REDUX.OR + FLO), so a pass costs no shuffle chain.
+template <bool SCAT>  // SCAT: the warp's lanes hold scattered env ids (reset_kernel)
 __device__ __noinline__ void draw_coop(Smem &sm, const Lane &L, const StepParams &p, int tid, int lane,
                                           uint64_t block0, bool do_draw, uint32_t x0, uint32_t y0, uint32_t base,
                                           uint32_t n, bool vfw, uint32_t quirks) {
@@ -284,13 +285,17 @@ __device__ __noinline__ void draw_coop(Smem &sm, const Lane &L, const StepParams
       r = k - cex;
     }
     const uint64_t dj = __shfl_sync(kFull, L.dirty, j);
+    // owner's RAM backing: env block0 + wl + j, or (SCAT) the owner lane's own pointer
+    const uint8_t *rj = SCAT ? reinterpret_cast<const uint8_t *>(
+                                   __shfl_sync(kFull, reinterpret_cast<unsigned long long>(L.ram), j))
+                             : p.s.ram + (block0 + wl + j) * 4096ull;
     bool hit = false;
     if (k < total) {
       const uint32_t pj = sm.dprm[warp][j];
       const uint32_t xj = pj & 63u, yy = (((pj >> 6) & 31u) + r) & 31u, a = (pj >> 11) + r;
       uint32_t byte = 0;
       if (a <= 0xFFFu)
-        byte = ((dj >> (a >> 6)) & 1ull) ? (uint32_t)p.s.ram[(block0 + wl + j) * 4096ull + a] : (uint32_t)sm.img[a];
+        byte = ((dj >> (a >> 6)) & 1ull) ? (uint32_t)rj[a] : (uint32_t)sm.img[a];
       uint64_t m = (uint64_t)byte << 56;
       m = bswap64(wrap ? ((m >> xj) | (xj ? (m << (64u - xj)) : 0ull)) : (m >> xj));
       uint64_t *row = &sm.fb[fb_idx(wl + j, yy)];
@@ -355,7 +360,8 @@ __device__ __forceinline__ void draw_lanes(Smem &sm, Lane &L, const StepParams &
 // warp's largest row count) publish packed parameters to a per-warp smem slot by rank;
 // lane r of group g XORs row r of drawer g, so all drawers cost one row step.  The
 // collision bits come back with one ballot.  dm = lanes with >= 1 row; DXY0 -> VF = 0.
-template <bool DIRTY>  // DIRTY: some lane of the warp has private RAM (sprite bytes may live in HBM)
+template <bool DIRTY, bool SCAT>  // DIRTY: some lane of the warp has private RAM (sprite bytes may
+                                   // live in HBM); SCAT: scattered env ids (reset_kernel)
 __device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepParams &p, int tid, int lane,
                                             uint64_t block0, uint32_t dm, uint32_t x0, uint32_t y0, uint32_t base,
                                             uint32_t nrows, uint32_t m, bool wdirty, uint32_t quirks, bool vfw) {
@@ -372,14 +378,19 @@ __device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepP
   const uint32_t q = gv ? sm.dprm[warp][g] : 0u;
   const uint32_t own = q >> 27, oe = wl + own;
   uint64_t od = 0;
-  if (DIRTY) od = __shfl_sync(kFull, L.dirty, own);
+  const uint8_t *oram = nullptr;  // owner's RAM backing
+  if (DIRTY) {
+    od = __shfl_sync(kFull, L.dirty, own);
+    oram = SCAT ? reinterpret_cast<const uint8_t *>(__shfl_sync(kFull, reinterpret_cast<unsigned long long>(L.ram), own))
+                : p.s.ram + (block0 + oe) * 4096ull;
+  }
   bool hit = false;
   if (gv && r < ((q >> 23) & 15u)) {
     const uint32_t ox = q & 63u, a = ((q >> 11) & 0xFFFu) + r;
     uint32_t byte = 0;
     if (DIRTY) {
       if (a <= 0xFFFu)
-        byte = ((od >> (a >> 6)) & 1ull) ? (uint32_t)p.s.ram[(block0 + oe) * 4096ull + a] : (uint32_t)sm.img[a];
+        byte = ((od >> (a >> 6)) & 1ull) ? (uint32_t)oram[a] : (uint32_t)sm.img[a];
     } else {
       byte = a <= 0xFFFu ? (uint32_t)sm.img[a] : 0u;  // no global load on the common path
     }
@@ -422,7 +433,7 @@ __device__ __forceinline__ void draw_one(Smem &sm, const Lane &L, int tid, bool 
 // that halts, re-executes its faulting entry with no effect -- an invalid word's entry has no
 // effect flags and stays at its PC (E_BAD is in L.stay), a stack fault keeps PC and SP -- so
 // no run flag gates the core; L.run then only records "did not fault" for the timer tick.
-template <bool Q0, bool RF>
+template <bool Q0, bool RF, bool SCAT = false>
 __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, int tid, int lane, uint64_t block0,
                                       uint32_t gid, bool part, bool &wdirty) {
   const uint32_t quirks = Q0 ? 0u : p.quirks;  // Q0: modern profile specialisation
@@ -560,9 +571,9 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     if (maxr >= 3u && (uint32_t)__popc(dm) * maxr <= 32u)  // k drawers fit 32 / maxr groups
     {
       if (wdirty)
-        draw_groups<true>(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
+        draw_groups<true, SCAT>(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
       else
-        draw_groups<false>(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
+        draw_groups<false, SCAT>(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
     }
     else if (maxr == 1u) {
       if (wdirty) draw_one<true>(sm, L, tid, nrows != 0u, vx & 63u, y0, L.I & 0xFFFu, quirks, do_draw);
@@ -570,18 +581,18 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     } else if (maxr <= kLaneDrawMax)
       draw_lanes(sm, L, p, tid, do_draw, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
     else
-      draw_coop(sm, L, p, tid, lane, block0, do_draw, vx & 63u, y0, L.I & 0xFFFu, n, do_draw, quirks);
+      draw_coop<SCAT>(sm, L, p, tid, lane, block0, do_draw, vx & 63u, y0, L.I & 0xFFFu, n, do_draw, quirks);
     __syncwarp();
   }
 }
 
 // `frames` frames of ipf cycles + timer tick, for lanes with `part` (uniform loop counts)
-template <bool Q0>
+template <bool Q0, bool SCAT = false>
 __device__ __forceinline__ void run_frames(Smem &sm, Lane &L, const StepParams &p, int tid, int lane, uint64_t block0,
                                            uint32_t gid, bool part, uint32_t frames, bool &wdirty) {
   L.run = part && !L.halted;
   for (uint32_t f = 0; f < frames; ++f) {
-    for (uint32_t k = 0; k < p.ipf; ++k) cycle<Q0, true>(sm, L, p, tid, lane, block0, gid, part, wdirty);
+    for (uint32_t k = 0; k < p.ipf; ++k) cycle<Q0, true, SCAT>(sm, L, p, tid, lane, block0, gid, part, wdirty);
     if (L.run) {
       L.dt -= (L.dt != 0u);
       L.st -= (L.st != 0u);
@@ -816,6 +827,21 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       }
       __syncwarp();
     }
+    // Specs with startup segments: a reset runs frames of startup code, which inline would
+    // hold the whole warp for one lane; the done envs are appended (warp-aggregated) to a
+    // list instead, and reset_kernel, launched right after on the same stream, runs them
+    // packed 128 per CTA (stream order keeps the same-step reset of A10).
+    if (p.reset_ids != nullptr) {
+      const uint32_t m = __ballot_sync(kFull, resetting);
+      if (m) {
+        const int leader = __ffs(m) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(p.reset_count, (uint32_t)__popc(m));
+        base = __shfl_sync(kFull, base, leader);
+        if (resetting) p.reset_ids[base + (uint32_t)__popc(m & ((1u << lane) - 1u))] = (uint32_t)env;
+      }
+      resetting = false;
+    }
   } else {
     resetting = active;
     L.episode = 0;
@@ -833,6 +859,10 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
 
     if (resetting) {
       set_keys(L, 0u);
+      // a lane that faulted in a startup segment keeps the faulting PC in the frame loops;
+      // its stored PC is the word after it, as the fetch advanced it (a2, A17, A33), except
+      // for a fetch past 0xFFE (stored unchanged)
+      if (L.halted && L.pc <= 0xFFEu) L.pc += 2u;
       steps = 0;
       prev = eval(p.score, sm, L, tid);
       ep_ret = 0;
@@ -919,6 +949,86 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       }
     }
   }  if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem outlives the store
+}
+
+// ---------------------------------------------------------------- deferred resets (K3)
+// The envs the step kernel listed (done, spec with startup segments), 128 per CTA in a
+// grid-stride loop: power-on, the startup segments, the new episode's score baseline; then
+// the reset display goes to all four obs planes and ring slots and the state is stored.
+template <bool Q0>
+__global__ void __launch_bounds__(kBlock, kMinBlocks)
+reset_kernel(const __grid_constant__ StepParams p, uint8_t *__restrict__ obs) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  Smem &sm = *reinterpret_cast<Smem *>(smraw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t count = *p.reset_count;
+  if ((uint64_t)blockIdx.x * kBlock >= count) return;  // uniform per CTA
+  if (tid == 0) stage_issue(sm, p.s.image, nullptr);
+  __syncthreads();  // mbarrier initialised
+  stage_wait(sm);
+  uint64_t *obs64 = reinterpret_cast<uint64_t *>(obs);
+  for (uint64_t b0 = (uint64_t)blockIdx.x * kBlock; b0 < count; b0 += (uint64_t)gridDim.x * kBlock) {
+    const bool part = b0 + tid < count;
+    const uint64_t env = part ? p.reset_ids[b0 + tid] : 0u;
+    OCTAX_CHECK(env < p.n);
+    Lane L;
+    L.pc = 0x10000u; L.I = 0; L.sp = 0; L.dt = 0; L.st = 0; L.halted = 1; L.draw = 0; L.episode = 0;
+    set_keys(L, 0u);
+    L.dirty = 0; L.ram = p.s.ram + env * 4096ull; L.stk_dirty = 0;
+    L.dec = __ldg(p.s.dec + L.pc);
+    const uint32_t gid = (uint32_t)(p.env_offset + env);
+    if (part) {
+      L.episode = p.s.ctrl[env].w;  // incremented by the step kernel
+      power_on(sm, L, p, tid);
+    }
+    __syncwarp();
+    bool wdirty = false;
+    for (uint32_t seg = 0; seg < p.n_startup; ++seg) {
+      if (part) set_keys(L, p.startup_keys[seg]);
+      run_frames<Q0, true>(sm, L, p, tid, lane, 0, gid, part, p.startup_frames[seg], wdirty);
+    }
+    uint32_t prev = 0;
+    if (part) {
+      set_keys(L, 0u);
+      if (L.halted && L.pc <= 0xFFEu) L.pc += 2u;  // faulted in startup: PC after the fetch (A33)
+      prev = eval(p.score, sm, L, tid);
+    }
+    __syncwarp();
+    // the reset display -> obs planes 0..3 and ring slots 0..3, one env per pass, lane = row
+    uint32_t wm = __ballot_sync(kFull, part);
+    while (wm) {
+      const int e = __ffs(wm) - 1;
+      wm &= wm - 1;
+      const uint64_t E = __shfl_sync(kFull, env, e);
+      const uint64_t v = sm.fb[fb_idx(warp * 32 + e, lane)];  // row `lane`
+      const uint32_t pos = (uint32_t)lane ^ (uint32_t)(E & kSwz);
+      for (uint32_t sl = 0; sl < 4; ++sl) ring_at(p, sl, E)[pos] = v;
+      if (obs64) {
+        uint64_t *ob = obs64 + E * 128 + lane;
+        __stcs(ob, v);
+        __stcs(ob + 32, v);
+        __stcs(ob + 64, v);
+        __stcs(ob + 96, v);
+      }
+    }
+    if (part) {
+      uint32_t w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) w[j] = *reinterpret_cast<const uint32_t *>(&sm.V[vbase(tid) | (j << 7)]);
+      p.s.regs[env] = make_uint4(w[0], w[1], w[2], w[3]);
+      p.s.ctrl[env] = make_uint4((L.pc & 0xFFFFu) | (L.I << 16), L.sp | (L.dt << 8) | (L.st << 16) | (L.halted << 24),
+                                 L.draw, L.episode);
+      p.s.book[env] = make_uint4(0u, prev, 0u, 0u);
+      uint32_t sw[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        sw[k] = (uint32_t)sm.stk[(2 * k) * kBlock + tid] | ((uint32_t)sm.stk[(2 * k + 1) * kBlock + tid] << 16);
+      p.s.stack[env * 2] = make_uint4(sw[0], sw[1], sw[2], sw[3]);
+      p.s.stack[env * 2 + 1] = make_uint4(sw[4], sw[5], sw[6], sw[7]);
+      p.s.dirty[env] = L.dirty;
+    }
+    __syncwarp();
+  }
 }
 
 // ---------------------------------------------------------------- auxiliary kernels
@@ -1063,12 +1173,39 @@ static cudaError_t launch_variant(const StepParams &p, const int32_t *actions, u
   return cudaGetLastError();
 }
 
+template <bool Q0>
+static cudaError_t launch_resets(const StepParams &p, uint8_t *obs, cudaStream_t stream) {
+  static std::atomic<uint64_t> attr_set{0};
+  const size_t smem = sizeof(Smem);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_set.load(std::memory_order_relaxed) & bit)) {
+    e = cudaFuncSetAttribute(reset_kernel<Q0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set.fetch_or(bit, std::memory_order_relaxed);
+  }
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t need = (p.n + kBlock - 1) / kBlock, cap = (uint64_t)sms * kMinBlocks;
+  reset_kernel<Q0><<<(unsigned)(need < cap ? need : cap), kBlock, smem, stream>>>(p, obs);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_step(const StepParams &p, int mode, const int32_t *actions, uint8_t *obs, float *reward,
                         uint8_t *done, uint8_t *term, uint8_t *trunc, cudaStream_t stream) {
   const bool q0 = p.quirks == 0u;
-  if (mode == MODE_STEP)
-    return q0 ? launch_variant<MODE_STEP, true>(p, actions, obs, reward, done, term, trunc, stream)
-              : launch_variant<MODE_STEP, false>(p, actions, obs, reward, done, term, trunc, stream);
+  if (mode == MODE_STEP) {
+    if (p.reset_ids) {  // deferred resets: count from zero, step, then the listed resets
+      cudaError_t e = cudaMemsetAsync(p.reset_count, 0, sizeof(uint32_t), stream);
+      if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = q0 ? launch_variant<MODE_STEP, true>(p, actions, obs, reward, done, term, trunc, stream)
+                       : launch_variant<MODE_STEP, false>(p, actions, obs, reward, done, term, trunc, stream);
+    if (e != cudaSuccess || !p.reset_ids) return e;
+    return q0 ? launch_resets<true>(p, obs, stream) : launch_resets<false>(p, obs, stream);
+  }
   return q0 ? launch_variant<MODE_RESET, true>(p, nullptr, obs, nullptr, nullptr, nullptr, nullptr, stream)
             : launch_variant<MODE_RESET, false>(p, nullptr, obs, nullptr, nullptr, nullptr, nullptr, stream);
 }

@@ -120,6 +120,19 @@ def test_frame_skip_ipf_variants_parity():
     _run_parity(rom, spec, 64, 60, 9, 9)
 
 
+@pytest.mark.parametrize("quirks", [0, 31])
+def test_deferred_reset_parity(quirks):
+    """Specs with startup segments reset their done envs in reset_kernel, after the step
+    kernel: fuzz ROMs (faults, self-modifying stores, so dirty-RAM sprite reads
+    inside startup frames), short episodes so most steps reset some envs, ragged n (3 CTAs)."""
+    rom = workloads.gen.fuzz_rom(77 + quirks, n_instr=240)
+    spec = dict(workloads.DEFAULTS, score="V0 + mem[0x300]", terminated="V3 == 7",
+                action_keys=list(range(16)), quirks=quirks, max_episode_steps=9,
+                startup=[(1 << 3, 3), (0, 2)])
+    g, _ = _run_parity(rom, spec, 300, 60, 5 + quirks, 6, check_every=10)
+    assert g.stats()[0][1] > 300  # episodes finished: the deferred path ran
+
+
 def test_reset_parity_and_obs():
     rom, spec = workloads.game("pong_standin", startup=[(2, 5)])
     g = _gpu_env(rom, spec, 50, 4)
