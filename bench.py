@@ -153,6 +153,20 @@ def oracle_throughput(game: str, envs_per_proc: int, steps: int, procs: int | No
     return [total / w for w in worst], C, sample
 
 
+def arm_config(args, spec, n, world):
+    """The bench line's `config`; both arms print this same dict (the reference arm
+    describes its bounded CPU sample under `cpu_baseline.sample`)."""
+    return {"workload": f"BASELINE configs[4] per-GPU slice: {args.game} (labelled stand-in ROM, "
+                        f"paper Pong spec P:152/P:156), {n} envs per GPU, frame_skip 4, ipf 12, "
+                        "uniform random actions (device Philox generator), packed 4-plane obs",
+            "game": args.game, "envs_per_gpu": n, "global_envs": world * n,
+            "frame_skip": spec["frame_skip"], "instructions_per_frame": spec["instructions_per_frame"],
+            "obs_format": "packed [n,4,32,8]" if args.obs == "packed" else "bool [n,4,64,32] (x-major, P:146)",
+            "parallelism": f"env-sharded x{world}",
+            "l2": f"inputs larger than L2: ~{ALG_BYTES_PER_ENV_STEP * n / 2**30:.2f} GiB "
+                  "touched per step vs 126 MB L2 (no flush needed)"}
+
+
 def run_reference(args):
     """--impl reference: the oracle (this tier's reference arm) on the host cores,
     same game / metric / unit as our arm; each step = one bounded sample round."""
@@ -160,6 +174,8 @@ def run_reference(args):
     if rank != 0:
         return 0
     envs_per_proc, steps_per_round = 256, 25
+    import workloads
+    _, spec = workloads.game(args.game, obs_format=1 if args.obs == "bool" else 0)
     vals, C, sample = oracle_throughput(args.game, envs_per_proc, steps_per_round,
                                         procs=args.cpu_procs, rounds=args.warmup + args.steps)
     timed = sorted(vals[args.warmup:])
@@ -169,9 +185,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": C * envs_per_proc * steps_per_round / v * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"{args.game} (same ROM/spec/actions recipe as our arm), CPU oracle on host cores, "
-                               "bounded sample per step", "game": args.game, "envs_per_process": envs_per_proc,
-                   "steps_per_round": steps_per_round},
+        "config": arm_config(args, spec, args.envs, _env_int("WORLD_SIZE", 1)),
         "cpu_baseline": {"value": v, "unit": "env steps/s", "cores": C, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": "env steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "frames_per_s": 4 * v,
@@ -438,14 +452,7 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"BASELINE configs[4] per-GPU slice: {args.game} (labelled stand-in ROM, "
-                                   f"paper Pong spec P:152/P:156), {n} envs per GPU, frame_skip 4, ipf 12, "
-                                   "uniform random actions (device Philox generator), packed 4-plane obs",
-                       "game": args.game, "envs_per_gpu": n, "global_envs": world * n,
-                       "frame_skip": spec["frame_skip"], "instructions_per_frame": spec["instructions_per_frame"],
-                       "obs_format": "packed [n,4,32,8]" if args.obs == "packed" else "bool [n,4,64,32] (x-major, P:146)", "parallelism": f"env-sharded x{world}",
-                       "l2": f"inputs larger than L2: ~{ALG_BYTES_PER_ENV_STEP * n / 2**30:.2f} GiB "
-                             "touched per step vs 126 MB L2 (no flush needed)"},
+            "config": arm_config(args, spec, n, world),
             "roofline": ({"bound": "alu", "achieved": alu["achieved"], "peak": alu["peak"], "unit": alu["unit"],
                           "frac": alu["frac"], "traffic": traffic, "kernel": "octax_kernel<MODE_STEP>",
                           "kernel_ms_median": kernel_ms, "alu": alu, "issue": issue,

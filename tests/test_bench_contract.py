@@ -33,6 +33,10 @@ def test_reference_arm_json_line():
     assert cb["kind"] == "oracle" and cb["cores"] == 2 and cb["value"] == d["value"] and cb["sample"]
     e = d["e2e"]
     assert e["value"] == d["value"] and e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
+    # same `config` dict as our arm (bench.arm_config), so the driver compares like with like
+    c = d["config"]
+    assert c["game"] == "pong_standin" and c["envs_per_gpu"] == 1048576 and c["global_envs"] == 1048576
+    assert c["frame_skip"] == 4 and c["instructions_per_frame"] == 12 and c["workload"].startswith("BASELINE configs[4]")
 
 
 def test_reference_arm_nonzero_rank_is_silent():
