@@ -602,3 +602,14 @@ def test_decode_totality_gpu(quirks):
         for j in ids:
             if not np.array_equal(gs[j - lo], o.get_state(j)):
                 raise AssertionError(f"state differs for word {j:04X}")
+
+
+def test_font_bytes_golden_gpu():
+    """The CUDA path's power-on image holds SURVEY App. B's 80 font bytes (tests/golden/font.txt)
+    -- its table is a transcription independent of the oracle's, so both are pinned to the golden."""
+    from tests.helpers import golden_lines
+    font = bytes(int(b, 16) for line in golden_lines("font.txt") for b in line.split()[1:])
+    rom, spec = workloads.game("pong_standin")
+    g = _gpu_env(rom, spec, 3, 1)
+    for c in g.get_states([0, 2]):
+        assert bytes(oracle.canon_fields(c)["mem"][0x50:0xA0]) == font

@@ -67,6 +67,76 @@ def test_cxnn_uses_philox_mapping():
         assert f["draw"] == 2
 
 
+def _mapping(kind):
+    for line in golden_lines("philox_mapping.txt"):
+        tok = line.split()
+        if tok[0] == kind:
+            yield tok[1:]
+
+
+def test_cxnn_mapping_golden_incl_episode_and_gid():
+    """SURVEY App. C mapping vectors (tests/golden/philox_mapping.txt): CXNN run by the
+    oracle from a set state with the given draw / episode counters and global id (env
+    offset) stores exactly the golden byte, so a counter slot swap (draw <-> episode,
+    gid in the wrong word) or a wrong domain fails here."""
+    rows = list(_mapping("cxnn"))
+    assert len(rows) == 5
+    for seed, draw, ep, gid, dom, out0, byte in rows:
+        seed, draw, ep, gid, dom = (int(v) for v in (seed, draw, ep, gid, dom))
+        assert oracle.philox4x32_10([draw, ep, gid, dom], [seed & 0xFFFFFFFF, seed >> 32])[0] == int(out0, 16)
+        if dom != 0:
+            continue
+        e = oracle.OracleEnv(SELF_JUMP, dict(BASE_SPEC), 1, seed, gid)
+        f = oracle.canon_fields(e.get_state(0))
+        mem = f["mem"]
+        mem[0x300], mem[0x301] = 0xC7, 0xFF                 # C7FF: V7 = byte & 0xFF
+        e.set_state(0, canon(PC=0x300, draw=draw, episode=ep, mem=mem))
+        e.run_cycles(0, 1)
+        g = oracle.canon_fields(e.get_state(0))
+        assert g["V"][7] == int(byte, 16), (draw, ep, gid)
+        assert g["draw"] == draw + 1 and g["episode"] == ep
+
+
+def test_cxnn_episode_counter_after_auto_reset():
+    """The episode slot advances on auto-reset (c.1 step: episode += 1; reset draws restart
+    at 0): a startup frame that runs CXNN gives the golden byte of episode 0 at create and of
+    episode 1 after the first (always-terminating) step, seed 42, gid 0 (App. C)."""
+    want = {int(r[2]): int(r[6], 16) for r in _mapping("cxnn")
+            if r[0] == "42" and r[1] == "0" and r[3] == "0" and r[4] == "0"}
+    rom = bytes([0xC1, 0xFF, 0x12, 0x02])                 # C1FF ; 1202 (self-jump)
+    e = oracle.OracleEnv(rom, dict(BASE_SPEC, terminated="1", startup=[(0, 1)]), 1, 42, 0)
+    f = oracle.canon_fields(e.get_state(0))
+    assert (f["V"][1], f["episode"], f["draw"]) == (want[0], 0, 1)
+    _, _, done, term, _ = e.step(np.zeros(1, np.int32))
+    assert done[0] == 1 and term[0] == 1
+    f = oracle.canon_fields(e.get_state(0))
+    assert (f["V"][1], f["episode"], f["draw"]) == (want[1], 1, 1)
+
+
+def test_action_stream_golden_table():
+    """SURVEY App. C synthetic action table (aseed 42, gids 0-2, t 0-3): out0 and its
+    residues mod 3 (Pong) and mod 17 (coverage ROM)."""
+    rows = list(_mapping("action"))
+    assert len(rows) == 12
+    for aseed, gid, t, out0, m3, m17 in rows:
+        aseed, gid, t = int(aseed), int(gid), int(t)
+        assert oracle.philox4x32_10([t, 0, gid, 1], [aseed, 0])[0] == int(out0, 16)
+        assert oracle.synthetic_action(aseed, t, gid, 3) == int(m3)
+        assert oracle.synthetic_action(aseed, t, gid, 17) == int(m17)
+        assert oracle.synthetic_actions(aseed, t, [gid], 17)[0] == int(m17)
+
+
+def test_sampled_env_ids_golden():
+    """SURVEY App. C config-4 sampled ids (seed 42, n_total 262,144, domain 2, k = 0..4),
+    the recipe tests/test_gpu_parity.py uses to pick its sampled envs."""
+    rows = list(_mapping("sample"))
+    assert len(rows) == 5
+    for seed, ntot, k, gid in rows:
+        seed = int(seed)
+        out0 = oracle.philox4x32_10([int(k), 0, 0, 2], [seed & 0xFFFFFFFF, seed >> 32])[0]
+        assert out0 % int(ntot) == int(gid)
+
+
 def test_synthetic_action_definition():
     for t, gid in ((0, 0), (5, 3), (2**33 + 1, 99)):
         out0 = oracle.philox4x32_10([t & 0xFFFFFFFF, t >> 32, gid, 1], [42, 0])[0]
@@ -283,6 +353,34 @@ def test_draw_twice_restores_display_property():
         hits = sum(1 for r, byte in enumerate(spr) for c in range(8)
                    if (byte >> (7 - c)) & 1 and y0 + r < 32 and x0 + c < 64 and bits[y0 + r, x0 + c])
         assert vf1 == (1 if hits else 0)
+
+
+def _golden_font():
+    rows = [line.split() for line in golden_lines("font.txt")]
+    assert [int(r[0], 16) for r in rows] == list(range(16))
+    return bytes(int(b, 16) for r in rows for b in r[1:])
+
+
+def test_font_bytes_golden():
+    """All 80 font bytes at 0x050..0x09F equal SURVEY App. B (tests/golden/font.txt), so a
+    one-nibble typo in any glyph row of the oracle's table fails (A23)."""
+    font = _golden_font()
+    assert len(font) == 80 and font[0] == 0xF0          # S:66
+    f = oracle.canon_fields(_env().get_state(0))
+    assert bytes(f["mem"][0x50:0xA0]) == font
+    # FX29 addresses glyph VX & 15 at 0x50 + 5 * digit (App. A.4 / SURVEY App. A), and
+    # drawing it renders exactly the golden rows
+    e = _env()
+    for k in range(16):
+        mem = oracle.canon_fields(e.get_state(0))["mem"]
+        mem[0x200:0x206] = [0xF3, 0x29, 0xD1, 0x25, 0x12, 0x04]
+        V = [0] * 16
+        V[1], V[2], V[3] = 0, 0, 0x10 | k                  # high nibble ignored
+        e.set_state(0, canon(V=V, PC=0x200, mem=mem))
+        e.run_cycles(0, 2)
+        g = oracle.canon_fields(e.get_state(0))
+        assert g["I"] == 0x50 + 5 * k
+        assert bytes(g["display"].reshape(32, 8)[0:5, 0]) == font[5 * k:5 * k + 5]
 
 
 def test_font_glyph_render_matches_font_bytes():
