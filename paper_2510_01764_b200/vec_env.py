@@ -14,6 +14,14 @@ C ABI -- argument marshalling only, every step runs in liboctax.so:
   episodes' return ``r`` and length ``l`` (valid where ``info["episode"]["_r"]``).
 * observations are torch CUDA tensors: bool ``[n, 4, 64, 32]`` (P:146 axis order)
   when ``dense=True``, else the packed ``[n, 4, 32, 8]`` uint8 form.
+* aliasing: by default (``copy=False``) ``obs`` and ``info["final_obs"]`` are
+  zero-copy views of the library's persistent output buffers (the dense bool view
+  reinterprets the kernel's 0/1 bytes in place, no expansion copy), valid until the
+  next ``step`` / ``reset`` overwrites them -- the fast path for a learner that
+  consumes the batch before stepping again.  ``copy=True`` returns clones (the
+  Gymnasium habit of keeping observations across steps, e.g. in rollout buffers).
+  ``reward``, ``terminated``, ``truncated`` and ``info["episode"]`` are always fresh
+  tensors (n scalars each).
 * ``stack="steps"`` (default, reading A3): the 4 planes are the last 4 step-end
   displays; ``stack="frames"``: the displays after the last 4 emulated frames of
   the step (OCTAX_OBS_STACK_FRAMES).
@@ -42,7 +50,8 @@ class Discrete:
 
 class OctaxVecEnv:
     def __init__(self, rom: bytes, spec: dict, num_envs: int, seed: int = 0, device: int = 0,
-                 dense: bool = True, env_offset: int = 0, stream=None, stack: str = "steps"):
+                 dense: bool = True, env_offset: int = 0, stream=None, stack: str = "steps",
+                 copy: bool = False):
         import torch
         if stack not in ("steps", "frames"):
             raise ValueError(f"stack must be 'steps' or 'frames', got {stack!r}")
@@ -51,6 +60,7 @@ class OctaxVecEnv:
         self._env = OctaxEnv(rom, spec, num_envs, seed, device=device, env_offset=env_offset, stream=stream)
         self.num_envs = num_envs
         self.dense = dense
+        self.copy = copy
         self.single_observation_space = Box((4, 64, 32), "bool") if dense else Box((4, 32, 8), "uint8", 0, 255)
         self.single_action_space = Discrete(self._env.n_actions)
         dev = self._env.device
@@ -66,7 +76,12 @@ class OctaxVecEnv:
             return cls(f.read(), spec, num_envs, **kw)
 
     def _view(self, t):
-        return t.view(self.num_envs, *self.single_observation_space.shape).bool() if self.dense else t
+        """Zero-copy: the kernel writes 0/1 bytes, reinterpreted as torch.bool in place."""
+        import torch
+        v = t.view(self.num_envs, *self.single_observation_space.shape)
+        if self.dense:
+            v = v.view(torch.bool)
+        return v.clone() if self.copy else v
 
     def reset(self, seed: int | None = None):
         if seed is not None:
@@ -82,9 +97,9 @@ class OctaxVecEnv:
         d = done.bool()
         info = {
             "final_obs": self._view(self._final), "_final_obs": d,
-            "episode": {"r": self._ret, "l": self._len, "_r": d},
+            "episode": {"r": self._ret.clone(), "l": self._len.clone(), "_r": d},
         }
-        return self._view(obs), rew, self._env.terminated.bool(), self._env.truncated.bool(), info
+        return self._view(obs), rew.clone(), self._env.terminated.bool(), self._env.truncated.bool(), info
 
     def statistics(self):
         """Integer totals since reset: {sum of returns, episodes, env steps, error flags}."""

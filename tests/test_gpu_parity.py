@@ -613,3 +613,31 @@ def test_font_bytes_golden_gpu():
     g = _gpu_env(rom, spec, 3, 1)
     for c in g.get_states([0, 2]):
         assert bytes(oracle.canon_fields(c)["mem"][0x50:0xA0]) == font
+
+
+@pytest.mark.parametrize("dense", [True, False])
+def test_vec_env_zero_copy_and_copy_mode(dense):
+    """OctaxVecEnv's default obs is a zero-copy view of the library's output buffer (the bool
+    view reinterprets the kernel's 0/1 bytes: same data_ptr, no 8 KB/env expansion copy);
+    copy=True returns clones that survive the next step (Gymnasium rollout-buffer habit)."""
+    from paper_2510_01764_b200.vec_env import OctaxVecEnv
+    rom, spec = workloads.game("brix_standin", max_episode_steps=30)
+    n = 96
+    fast = OctaxVecEnv(rom, spec, n, seed=3, dense=dense)
+    safe = OctaxVecEnv(rom, spec, n, seed=3, dense=dense, copy=True)
+    obs, _ = fast.reset(seed=3)
+    assert obs.data_ptr() == fast._env.obs.data_ptr()
+    assert obs.dtype == (torch.bool if dense else torch.uint8)
+    sobs, _ = safe.reset(seed=3)
+    assert sobs.data_ptr() != safe._env.obs.data_ptr() and torch.equal(obs, sobs)
+    kept = []
+    for t in range(12):
+        a = torch.from_numpy(workloads.gen.actions(8, t, n, fast.single_action_space.n))
+        o1, r1, te1, tr1, i1 = fast.step(a)
+        o2, r2, te2, tr2, i2 = safe.step(a)
+        assert o1.data_ptr() == fast._env.obs.data_ptr()
+        assert i1["final_obs"].data_ptr() == fast._final.data_ptr()
+        assert torch.equal(o1, o2) and torch.equal(r1, r2) and torch.equal(te1, te2)
+        kept.append((o2, o1.clone(), i2["episode"]["r"], i1["episode"]["r"].clone()))
+    for o2, o1c, r2, r1c in kept:   # copies kept across steps are still the step's values
+        assert torch.equal(o2, o1c) and torch.equal(r2, r1c)
