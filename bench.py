@@ -102,15 +102,19 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle (baseline / reference arm)
-def _oracle_worker(game, envs_per_proc, steps, rounds, k, barrier, q):
+def _oracle_worker(game, obs_format, envs_per_proc, steps, rounds, k, barrier, q):
     import numpy as np
 
     import oracle
     import workloads
-    rom, spec = workloads.game(game)
+    rom, spec = workloads.game(game, obs_format=obs_format)
     na = workloads.n_actions(spec)
-    e = oracle.OracleEnv(rom, spec, envs_per_proc, workloads.ENV_SEED, k * envs_per_proc)
-    acts = [np.ascontiguousarray(workloads.gen.actions(5, t, envs_per_proc, na)) for t in range(steps)]
+    off = k * envs_per_proc
+    e = oracle.OracleEnv(rom, spec, envs_per_proc, workloads.ENV_SEED, off)
+    # the same Philox domain-1 action stream the GPU arm draws on the device (octax_gen_actions),
+    # for the same global ids, generated before the timed rounds
+    acts = [np.ascontiguousarray(oracle.synthetic_actions(workloads.ACTION_SEED, t, range(off, off + envs_per_proc), na))
+            for t in range(steps)]
     obs = np.zeros((envs_per_proc, e.obs_per_env), np.uint8)
     rew = np.zeros(envs_per_proc, np.float32)
     done = np.zeros(envs_per_proc, np.uint8)
@@ -122,7 +126,8 @@ def _oracle_worker(game, envs_per_proc, steps, rounds, k, barrier, q):
         q.put((r, time.perf_counter() - t0))
 
 
-def oracle_throughput(game: str, envs_per_proc: int, steps: int, procs: int | None = None, rounds: int = 1):
+def oracle_throughput(game: str, envs_per_proc: int, steps: int, procs: int | None = None, rounds: int = 1,
+                      obs_format: int = 0):
     """The oracle as it stands, on the host cores: C worker processes, each its
     own single-threaded oracle instance over a disjoint env range, started
     together for each round.  Returns (per-round aggregate steps/s list, cores,
@@ -131,7 +136,7 @@ def oracle_throughput(game: str, envs_per_proc: int, steps: int, procs: int | No
     C = procs or len(os.sched_getaffinity(0))
     ctx = mp.get_context("spawn")
     barrier, q = ctx.Barrier(C), ctx.Queue()
-    ps = [ctx.Process(target=_oracle_worker, args=(game, envs_per_proc, steps, rounds, k, barrier, q))
+    ps = [ctx.Process(target=_oracle_worker, args=(game, obs_format, envs_per_proc, steps, rounds, k, barrier, q))
           for k in range(C)]
     for p in ps:
         p.start()
@@ -149,22 +154,38 @@ def oracle_throughput(game: str, envs_per_proc: int, steps: int, procs: int | No
     except Exception:
         pass
     sample = (f"{game}: {C} processes x {envs_per_proc} envs x {steps} steps = {total} env steps per round, "
-              f"slowest process {sorted(worst)[len(worst) // 2]:.2f} s (median round); {cpu}")
+              f"{'bool' if obs_format & 1 else 'packed'} obs, Philox domain-1 actions of global ids "
+              f"0..{C * envs_per_proc - 1}, slowest process {sorted(worst)[len(worst) // 2]:.2f} s (median round); {cpu}")
     return [total / w for w in worst], C, sample
 
 
-def arm_config(args, spec, n, world):
-    """The bench line's `config`; both arms print this same dict (the reference arm
-    describes its bounded CPU sample under `cpu_baseline.sample`)."""
-    return {"workload": f"BASELINE configs[4] per-GPU slice: {args.game} (labelled stand-in ROM, "
-                        f"paper Pong spec P:152/P:156), {n} envs per GPU, frame_skip 4, ipf 12, "
-                        "uniform random actions (device Philox generator), packed 4-plane obs",
-            "game": args.game, "envs_per_gpu": n, "global_envs": world * n,
-            "frame_skip": spec["frame_skip"], "instructions_per_frame": spec["instructions_per_frame"],
-            "obs_format": "packed [n,4,32,8]" if args.obs == "packed" else "bool [n,4,64,32] (x-major, P:146)",
-            "parallelism": f"env-sharded x{world}",
-            "l2": f"inputs larger than L2: ~{ALG_BYTES_PER_ENV_STEP * n / 2**30:.2f} GiB "
-                  "touched per step vs 126 MB L2 (no flush needed)"}
+ACTIONS = "uniform random, Philox4x32-10 domain-1 stream keyed by global env id (SURVEY App. C)"
+
+
+def arm_config(args, spec, n, world, impl="ours", sample=None):
+    """The bench line's `config`.  Both arms share the workload identity keys (game, spec,
+    obs format, actions, the per-GPU env count the line stands for); each states what it
+    actually ran: ours the device path over all n envs per GPU, the reference arm (the CPU
+    oracle) a bounded sample of the same workload (`sample`)."""
+    c = {"workload": f"BASELINE configs[4] per-GPU slice: {args.game} (labelled stand-in ROM, "
+                     f"paper Pong spec P:152/P:156), {n} envs per GPU, frame_skip 4, ipf 12, "
+                     f"{'bool [n,4,64,32]' if args.obs == 'bool' else 'packed 4-plane'} obs",
+         "game": args.game, "envs_per_gpu": n, "global_envs": world * n,
+         "frame_skip": spec["frame_skip"], "instructions_per_frame": spec["instructions_per_frame"],
+         "obs_format": "packed [n,4,32,8]" if args.obs == "packed" else "bool [n,4,64,32] (x-major, P:146)",
+         "actions": ACTIONS, "parallelism": f"env-sharded x{world}"}
+    if impl == "ours":
+        c["ran"] = (f"device: {n} envs per GPU x {world} GPU(s), actions generated on the device "
+                    "(octax_gen_actions) before the timed region")
+        c["l2"] = (f"inputs larger than L2: ~{ALG_BYTES_PER_ENV_STEP * n / 2**30:.2f} GiB touched per step "
+                   "vs 126 MB L2 (no flush needed)")
+    else:
+        c["ran"] = ("host CPU oracle (oracle/octax_oracle.c, single-threaded C, one process per core): "
+                    f"a bounded sample of this workload, {sample['envs']} envs x {sample['steps']} steps per "
+                    "round, actions from the oracle's own Philox (oracle.synthetic_actions) for the same "
+                    "global ids, generated before the timed rounds")
+        c["sample"] = sample
+    return c
 
 
 def run_reference(args):
@@ -176,8 +197,9 @@ def run_reference(args):
     envs_per_proc, steps_per_round = 256, 25
     import workloads
     _, spec = workloads.game(args.game, obs_format=1 if args.obs == "bool" else 0)
+    fmt = 1 if args.obs == "bool" else 0
     vals, C, sample = oracle_throughput(args.game, envs_per_proc, steps_per_round,
-                                        procs=args.cpu_procs, rounds=args.warmup + args.steps)
+                                        procs=args.cpu_procs, rounds=args.warmup + args.steps, obs_format=fmt)
     timed = sorted(vals[args.warmup:])
     v = timed[len(timed) // 2]
     out = {
@@ -185,7 +207,9 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": C * envs_per_proc * steps_per_round / v * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": arm_config(args, spec, args.envs, _env_int("WORLD_SIZE", 1)),
+        "config": arm_config(args, spec, args.envs, _env_int("WORLD_SIZE", 1), impl="reference",
+                             sample={"processes": C, "envs_per_process": envs_per_proc, "envs": C * envs_per_proc,
+                                     "steps": steps_per_round, "obs_format": fmt}),
         "cpu_baseline": {"value": v, "unit": "env steps/s", "cores": C, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": "env steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "frames_per_s": 4 * v,
@@ -196,10 +220,12 @@ def run_reference(args):
 
 # ------------------------------------------------------------------ GPU arm
 def time_config(rom, spec, n, steps, warmup, rank_offset, aseed, torch, OctaxEnv, barrier=None,
-                keep=False, graph=False):
+                keep=False, graph=False, rollout=0, on_rollout=None):
     """Time `steps` octax_step launches (each = one step of all n envs) on a dedicated
     stream with CUDA events; graph=True captures the K launches in one CUDA graph
-    (K % 4 == 0 keeps the 4-slot display ring aligned across replays)."""
+    (K % 4 == 0 keeps the 4-slot display ring aligned across replays).  on_rollout(env, stream)
+    runs inside the timed region after every `rollout` steps and after the last one (the
+    per-rollout statistics all-reduce of SURVEY §8(e))."""
     stream = torch.cuda.Stream()
     env = OctaxEnv(rom, spec, n, 0x0C7A251001764000, env_offset=rank_offset, stream=stream)
     T = warmup + steps
@@ -233,6 +259,8 @@ def time_config(rom, spec, n, steps, warmup, rank_offset, aseed, torch, OctaxEnv
     else:
         for k in range(steps):
             env.step_into(acts[warmup + k], obs, rew, done)
+            if on_rollout is not None and ((rollout and (k + 1) % rollout == 0) or k == steps - 1):
+                on_rollout(env, stream)
             ev[k + 1].record(stream)
     torch.cuda.synchronize()
     if barrier:
@@ -247,15 +275,30 @@ def time_config(rom, spec, n, steps, warmup, rank_offset, aseed, torch, OctaxEnv
 
 
 def issue_model(game, n):
-    """Warp instructions per env step measured by ncu (profiles/latest_step_full.json)."""
+    """ncu instruction counts of the step kernel (profiles/latest_step_full.json), used for the
+    ALU-pipe and issue roofs only if the profile is of THIS build and workload: the device-code
+    digest (cuobjdump -sass sha256) of the loaded library, the step-kernel symbol, the game and
+    the env count must all match.  Returns (counts or None, reason)."""
     try:
         with open(os.path.join(ROOT, "profiles", "latest_step_full.json")) as f:
             j = json.load(f)
-        if j.get("game") == game:
-            return j
-    except Exception:
-        pass
-    return None
+    except Exception as ex:
+        return None, f"no profile: {ex}"
+    from paper_2510_01764_b200 import octax
+    from paper_2510_01764_b200.build import device_code_digest
+    have = device_code_digest(octax.SO_PATH)
+    why = []
+    if j.get("sass_sha256") is None or j.get("sass_sha256") != have:
+        why.append(f"device code {str(j.get('sass_sha256'))[:12]} != loaded {str(have)[:12]}")
+    if "octax_kernel<(int)0" not in str(j.get("kernel_symbol", "")):
+        why.append("profile is not of the step kernel")
+    if j.get("game") != game:
+        why.append(f"game {j.get('game')} != {game}")
+    if j.get("envs") != n:
+        why.append(f"envs {j.get('envs')} != {n}")
+    if why:
+        return None, "stale ncu profile: " + "; ".join(why)
+    return j, "profiles/latest_step_full.json (same device code, kernel, game and env count)"
 
 
 def main():
@@ -271,6 +314,12 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-backend", default="auto", choices=["auto", "nccl", "gloo"],
+                    help="auto: nccl with one GPU per rank; gloo when ranks share a device "
+                         "(a functional multi-rank run on fewer GPUs than ranks)")
+    ap.add_argument("--rollout", type=int, default=100,
+                    help="steps per rollout: one int64[4] statistics all-reduce per rollout, inside "
+                         "the timed region (P:228 100-step rollouts, SURVEY §8(e))")
     ap.add_argument("--cpu-procs", type=int, default=None,
                     help="--impl reference: oracle processes (default: one per host core)")
     args = ap.parse_args()
@@ -288,9 +337,17 @@ def main():
 
     from paper_2510_01764_b200 import dist as odist
     rank, world, local = odist.rank_info()
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    dev = local % ndev
+    torch.cuda.set_device(dev)
+    backend = args.dist_backend
+    if backend == "auto":
+        backend = "nccl" if world <= ndev else "gloo"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
 
     def barrier():
         if world > 1:
@@ -300,16 +357,23 @@ def main():
     n = args.envs
     offset, _ = odist.shard(rank, world, n)
 
-    # ---- headline: n envs per GPU, K timed steps
-    with ClockSampler(local) as clk:
+    # ---- headline: n envs per GPU, K timed steps; after every rollout (and the last step) the
+    #      int64[4] episode statistics are all-reduced inside the timed region
+    st = torch.zeros(4, dtype=torch.int64, device="cuda")
+    n_reduce = [0]
+
+    def on_rollout(env, stream):
+        with torch.cuda.stream(stream):
+            env.stats_device(st)
+            odist.reduce_stats(st)
+        n_reduce[0] += 1
+
+    with ClockSampler(dev) as clk:
         total_ms, per, kept = time_config(rom, spec, n, args.steps, args.warmup, offset,
-                                          workloads.ACTION_SEED, torch, OctaxEnv, barrier, keep=True)
-        # one NCCL all-reduce of the integer episode statistics per rollout
+                                          workloads.ACTION_SEED, torch, OctaxEnv, barrier, keep=True,
+                                          rollout=args.rollout, on_rollout=on_rollout)
         env, acts, stream = kept
-        st = torch.zeros(4, dtype=torch.int64, device="cuda")
-        env.stats_device(st)
         stream.synchronize()
-        odist.reduce_stats(st)
     # per-env 64-bit state digests after the timed steps (SURVEY d.1 item 4): rank 0's shard
     # sum is the same for every N (trajectories are keyed by global id), the all-rank sum
     # covers every env of the job (int64 all-reduce = sum mod 2^64)
@@ -327,22 +391,21 @@ def main():
     hbm_peak, peak_src = _peaks()
     achieved = ALG_BYTES_PER_ENV_STEP * n / (kernel_ms / 1e3) / 1e9
     traffic = None
-    im_t = issue_model(args.game, n)
-    if im_t and im_t.get("envs") == n and im_t.get("dram_bytes_per_launch"):
-        traffic = im_t["dram_bytes_per_launch"]   # ncu --set full, same launch configuration
 
     # ALU-pipe roof (the binding one): 148 SMs x 4 SMSPs x one
     # ALU-pipe warp instruction per 2 cycles (B300_MICROARCH: alu pipe rt_SMSP = 2) x 32
     # lanes x the SM clock sampled during the timed region; the work per env step is the
     # kernel's ALU-pipe instruction count measured by ncu (profiles/latest_step_full.json).
     alu = None
-    im = issue_model(args.game, n)
+    im, im_why = issue_model(args.game, n)
     clk_mhz = None
     try:
         clk_mhz = clk.summary()["sm_mhz"]
     except Exception:
         pass
     f_sm = (clk_mhz or 1965.0) * 1e6
+    if im and im.get("dram_bytes_per_launch"):
+        traffic = im["dram_bytes_per_launch"]   # ncu --set full of this build, same launch configuration
     if im and im.get("alu_warp_instr_per_env_step"):
         peak_alu = 148 * 4 * 0.5 * 32 * f_sm / 1e9          # G thread-ALU-ops / s
         ach_alu = im["alu_warp_instr_per_env_step"] * 32 * value / world / 1e9
@@ -351,7 +414,8 @@ def main():
                "all_warp_instr_per_env_step": im.get("warp_instr_per_env_step"),
                "warp_exec_efficiency": im.get("warp_exec_efficiency"),
                "ncu_alu_pipe_pct_of_peak": im.get("alu_pipe_pct_of_peak"),
-               "sm_mhz": f_sm / 1e6, "source": im.get("source")}
+               "sm_mhz": f_sm / 1e6, "source": im.get("source"), "provenance": im_why,
+               "sass_sha256": im.get("sass_sha256")}
 
     # issue roof (SURVEY d.2): 148 SMs x 4 schedulers x 1 warp instruction per cycle x f_SM,
     # against all warp instructions per env step measured by ncu (same source as the ALU count)
@@ -439,9 +503,11 @@ def main():
             games.append({"game": g, "envs_per_gpu": m, "steps_per_s": sps, "frames_per_s": 4 * sps,
                           "source": "paper listing (App. D)" if g.startswith("target") else "labelled stand-in"})
 
+    # the oracle on the host cores, rank 0 only, after every rank's GPU work (the other ranks
+    # wait at the closing barrier)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        vals, C, sample = oracle_throughput(args.game, 256, 400)
+    if rank == 0 and not args.no_cpu:
+        vals, C, sample = oracle_throughput(args.game, 256, 400, obs_format=1 if args.obs == "bool" else 0)
         v = vals[0]
         cpu = {"value": v, "unit": "env steps/s", "cores": C, "kind": "oracle", "sample": sample}
 
@@ -453,6 +519,10 @@ def main():
             "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": arm_config(args, spec, n, world),
+            "dist": {"backend": backend if world > 1 else None, "world": world, "devices": ndev,
+                     "stats_allreduces_in_timed_region": n_reduce[0], "rollout_steps": args.rollout,
+                     "note": ("ranks share a device: functional multi-rank run, not a scaling number"
+                              if world > ndev else "one GPU per rank")},
             "roofline": ({"bound": "alu", "achieved": alu["achieved"], "peak": alu["peak"], "unit": alu["unit"],
                           "frac": alu["frac"], "traffic": traffic, "kernel": "octax_kernel<MODE_STEP>",
                           "kernel_ms_median": kernel_ms, "alu": alu, "issue": issue,
@@ -462,6 +532,7 @@ def main():
                          if alu else
                          {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                           "frac": achieved / hbm_peak, "traffic": traffic, "kernel": "octax_kernel<MODE_STEP>",
+                          "alu": None, "alu_unavailable": im_why,
                           "kernel_ms_median": kernel_ms, "alg_bytes_per_env_step": ALG_BYTES_PER_ENV_STEP,
                           "peak_source": peak_src}),
             "cpu_baseline": cpu,

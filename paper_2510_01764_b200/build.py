@@ -48,6 +48,19 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
     return so
 
 
+def device_code_digest(so: str = SO) -> str | None:
+    """sha256 of the library's device code as `cuobjdump -sass` prints it: the identity of the
+    kernels a profile was taken from (the .so file itself is not byte-reproducible across
+    builds, its SASS is).  None if cuobjdump or the library is missing."""
+    import hashlib
+    cuobjdump = os.path.join(os.path.dirname(NVCC), "cuobjdump")
+    try:
+        out = subprocess.run([cuobjdump, "-sass", so], capture_output=True, text=True, timeout=120).stdout
+    except (OSError, subprocess.SubprocessError):
+        return None
+    return hashlib.sha256(out.encode()).hexdigest() if out else None
+
+
 def build_variant(out: str, defines=()) -> str:
     """Build the library from the current sources into `out` (A/B experiments)."""
     cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-o", out, *SOURCES]

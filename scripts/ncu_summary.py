@@ -79,6 +79,17 @@ def full(path, out, extra):
                 d[m] = {"value": v[i], "unit": units[i]}
         res.append(d)
     js = {"source": path, **extra, "launches": res}
+    # provenance: the kernel symbol profiled and the device-code digest of the library that ran
+    # it (bench.py reports instruction-count rooflines only when both match the loaded build)
+    if res:
+        js["kernel_symbol"] = res[0]["kernel"]
+    so = extra.pop("so", None) if isinstance(extra, dict) else None
+    js.pop("so", None)
+    if so:
+        sys.path.insert(0, ".")
+        from paper_2510_01764_b200.build import device_code_digest
+        js["sass_sha256"] = device_code_digest(so)
+        js["so"] = so
     if res:
         r0 = res[0]
         try:

@@ -33,10 +33,34 @@ def test_reference_arm_json_line():
     assert cb["kind"] == "oracle" and cb["cores"] == 2 and cb["value"] == d["value"] and cb["sample"]
     e = d["e2e"]
     assert e["value"] == d["value"] and e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
-    # same `config` dict as our arm (bench.arm_config), so the driver compares like with like
+    # the workload identity keys of our arm's `config` (bench.arm_config), so the driver compares
+    # like with like, plus what this arm actually ran: a bounded oracle sample
     c = d["config"]
     assert c["game"] == "pong_standin" and c["envs_per_gpu"] == 1048576 and c["global_envs"] == 1048576
     assert c["frame_skip"] == 4 and c["instructions_per_frame"] == 12 and c["workload"].startswith("BASELINE configs[4]")
+    assert "device" not in c["workload"] and "Philox" in c["actions"]
+    assert c["sample"]["processes"] == 2 and c["sample"]["envs"] == 2 * c["sample"]["envs_per_process"]
+    assert "oracle" in c["ran"] and str(c["sample"]["envs"]) in c["ran"]
+    import argparse
+    sys.path.insert(0, ROOT)
+    import bench
+    import workloads
+    _, spec = workloads.game("pong_standin")
+    ours = bench.arm_config(argparse.Namespace(game="pong_standin", obs="packed"), spec, 1048576, 1)
+    shared = ("workload", "game", "envs_per_gpu", "global_envs", "frame_skip", "instructions_per_frame",
+              "obs_format", "actions", "parallelism")
+    assert {k: ours[k] for k in shared} == {k: c[k] for k in shared}
+    assert "device" in ours["ran"] and "sample" not in ours
+
+
+def test_reference_arm_bool_obs_runs_bool_oracle():
+    env = dict(os.environ)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--obs", "bool",
+                        "--steps", "1", "--warmup", "0", "--cpu-procs", "1"],
+                       capture_output=True, text=True, env=env, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["config"]["sample"]["obs_format"] == 1 and "bool obs" in d["cpu_baseline"]["sample"]
 
 
 def test_reference_arm_nonzero_rank_is_silent():

@@ -641,3 +641,87 @@ def test_vec_env_zero_copy_and_copy_mode(dense):
         kept.append((o2, o1.clone(), i2["episode"]["r"], i1["episode"]["r"].clone()))
     for o2, o1c, r2, r1c in kept:   # copies kept across steps are still the step's values
         assert torch.equal(o2, o1c) and torch.equal(r2, r1c)
+
+
+# ---------------------------------------------------------------- full-size sampled parity helper
+def _sampled_parity(rom, spec, n, T, extra_ids=(), check_every=None):
+    """n envs on the GPU with device-generated actions; the SURVEY d.1 config-4 sample
+    ({0, 1, n/2, n-1} + 60 Philox domain-2 ids + extra_ids) re-simulated one oracle instance
+    each; obs / reward / done gathered on device every step, final canonical states compared
+    (and every `check_every` steps)."""
+    na = workloads.n_actions(spec)
+    g = _gpu_env(rom, spec, n, workloads.ENV_SEED)
+    a = torch.empty(n, dtype=torch.int32, device="cuda")
+    key = [workloads.ENV_SEED & 0xFFFFFFFF, workloads.ENV_SEED >> 32]
+    ids = [0, 1, n // 2, n - 1] + [oracle.philox4x32_10([k, 0, 0, 2], key)[0] % n for k in range(60)]
+    ids += [i for i in extra_ids if i < n]
+    oracles = [oracle.OracleEnv(rom, spec, 1, workloads.ENV_SEED, gid) for gid in ids]
+    idx = torch.tensor(ids, device="cuda")
+    dones = 0
+    for t in range(T):
+        g.gen_actions(workloads.ACTION_SEED, t, a)
+        obs, rew, done = g.step(a)
+        go = obs.reshape(n, -1)[idx].cpu().numpy()
+        gr = rew[idx].cpu().numpy()
+        gd = done[idx].cpu().numpy()
+        dones += int(done.sum().item())
+        for k, gid in enumerate(ids):
+            act = np.array([oracle.synthetic_action(workloads.ACTION_SEED, t, gid, na)], np.int32)
+            oo, orw, od, _, _ = oracles[k].step(act)
+            assert np.array_equal(go[k], oo[0]) and gr[k] == orw[0] and gd[k] == od[0], (t, gid)
+        if check_every and (t + 1) % check_every == 0:
+            st = g.get_states(ids)
+            for k in range(len(ids)):
+                assert np.array_equal(st[k], oracles[k].get_state(0)), (t, ids[k])
+    st = g.get_states(ids)
+    for k in range(len(ids)):
+        assert np.array_equal(st[k], oracles[k].get_state(0)), ids[k]
+    s, rc = g.stats()
+    assert s[2] == n * T
+    return g, dones
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("game", ["pong_standin", "brix_standin"])
+def test_reset_kernel_multipass_sampled_parity(game):
+    """Deferred resets (specs with startup segments) when one step resets far more envs than
+    reset_kernel's grid holds (148 SMs x 5 CTAs x 128 = 94,720): all 262,144 envs were created
+    together and truncate on the same steps (max_episode_steps = 5), so steps 5 and 10 reset
+    every env in one launch -- 3 grid-stride passes reusing the CTA's shared-memory slots
+    (VERDICT r1 weak #2).  The config-4 sample plus ids around the pass-size
+    boundaries are compared step by step, full canonical state every 5 steps."""
+    rom, spec = workloads.game(game, startup=[(0, 3), (1 << 1, 2)], max_episode_steps=5)
+    n = 262144
+    passes = [94720 * k + j for k in range(3) for j in (0, 127, 128, 94719) if 94720 * k + j < n]
+    g, dones = _sampled_parity(rom, spec, n, 12, extra_ids=passes, check_every=5)
+    assert dones >= 2 * n  # the synchronized truncations happened
+    s, _ = g.stats()
+    assert s[1] >= 2 * n
+
+
+@pytest.mark.slow
+def test_bool_obs_1M_sampled_parity():
+    """OCTAX_OBS_BOOL_XMAJOR at the bench's 1,048,576 envs (the 8 KB/env expand_obs_kernel
+    path the bool-obs throughput is quoted on), 64 sampled envs vs the oracle's bool obs."""
+    rom, spec = workloads.game("pong_standin", obs_format=1)
+    _sampled_parity(rom, spec, 1 << 20, 24)
+
+
+@pytest.mark.slow
+def test_stack_frames_1M_sampled_parity():
+    """OCTAX_OBS_STACK_FRAMES (per-frame obs planes written inside the step kernel) at
+    1,048,576 envs, with truncation so same-step resets occur in the sample."""
+    rom, spec = workloads.game("brix_standin", obs_format=16, max_episode_steps=11)
+    _sampled_parity(rom, spec, 1 << 20, 24)
+
+
+@pytest.mark.parametrize("obs_format,quirks", [(16, 31), (17, 31), (16, 0)])
+def test_stack_frames_startup_quirks_parity(obs_format, quirks):
+    """OCTAX_OBS_STACK_FRAMES x startup segments (deferred resets writing the reset display to
+    all planes) x all quirks, ragged n, full state: the combination VERDICT r1 found untested."""
+    rom = workloads.gen.fuzz_rom(501 + quirks, n_instr=260)
+    spec = dict(workloads.DEFAULTS, score="V0 + mem[0x300]", terminated="V3 == 7",
+                action_keys=list(range(16)), quirks=quirks, max_episode_steps=13,
+                startup=[(1 << 5, 2), (0, 3)], obs_format=obs_format, frame_skip=3)
+    g, _ = _run_parity(rom, spec, 333, 60, 41 + quirks, 4, check_every=10)
+    assert g.stats()[0][1] > 333
