@@ -16,6 +16,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import re
 import subprocess
 import sys
 import threading
@@ -290,7 +291,7 @@ def issue_model(game, n):
     why = []
     if j.get("sass_sha256") is None or j.get("sass_sha256") != have:
         why.append(f"device code {str(j.get('sass_sha256'))[:12]} != loaded {str(have)[:12]}")
-    if "octax_kernel<(int)0" not in str(j.get("kernel_symbol", "")):
+    if not re.search(r"octax_kernel<(\(int\))?0,", str(j.get("kernel_symbol", ""))):
         why.append("profile is not of the step kernel")
     if j.get("game") != game:
         why.append(f"game {j.get('game')} != {game}")
@@ -320,6 +321,8 @@ def main():
     ap.add_argument("--rollout", type=int, default=100,
                     help="steps per rollout: one int64[4] statistics all-reduce per rollout, inside "
                          "the timed region (P:228 100-step rollouts, SURVEY §8(e))")
+    ap.add_argument("--max-episode-steps", type=int, default=None,
+                    help="override the game spec's truncation length (tests: force auto-resets)")
     ap.add_argument("--cpu-procs", type=int, default=None,
                     help="--impl reference: oracle processes (default: one per host core)")
     args = ap.parse_args()
@@ -354,6 +357,8 @@ def main():
             dist.barrier()
 
     rom, spec = workloads.game(args.game, obs_format=1 if args.obs == "bool" else 0)
+    if args.max_episode_steps is not None:
+        spec = dict(spec, max_episode_steps=args.max_episode_steps)
     n = args.envs
     offset, _ = odist.shard(rank, world, n)
 
