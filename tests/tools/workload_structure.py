@@ -110,11 +110,93 @@ def lockstep(game, warm=300, steps=40):
             "warp_skippable_cycles": tail / cyc, "draw_paths": {k: v / cyc for k, v in paths.items()}}
 
 
+def regroup(game, warm=300, steps=24, cta=128):
+    """SURVEY NEXT-2 (i) / VERDICT r1 #6: would regrouping a CTA's envs into warps by PC or by
+    opcode class (an intra-CTA lane -> env permutation over the shared-memory-resident state)
+    make warps uniform?  One CTA of `cta` envs (0..cta-1) is replayed cycle by cycle in the
+    oracle; every warp-cycle is scored under three groupings of the CTA into warps of 32:
+      identity      -- lane = env (the kernel as built);
+      frame-sorted  -- at every frame boundary the envs are sorted by PC (then by opcode
+                       class) and cut into warps; the grouping is held for the frame's cycles
+                       (the regrouping a kernel could afford: one permutation per frame);
+      cycle-sorted  -- re-sorted by the current PC at EVERY cycle (an upper bound no kernel
+                       reaches: it would move every env's state every cycle).
+    Scores: mean distinct PCs and distinct classes (high nibble; halted lanes = class -1) per
+    warp-cycle, and the share of warp-cycles that are PC-uniform / class-uniform."""
+    rom, spec = workloads.game(game)
+    ipf, fs = spec["instructions_per_frame"], spec["frame_skip"]
+    o = oracle.OracleEnv(rom, spec, cta, workloads.ENV_SEED)
+    na = workloads.n_actions(spec)
+    for t in range(warm):
+        o.step(workloads.gen.actions(workloads.ACTION_SEED, t, cta, na))
+    score = {g: {"pcs": 0.0, "cls": 0.0, "pc_uni": 0, "cls_uni": 0} for g in ("identity", "frame", "cycle")}
+    wc = 0
+
+    def peek():
+        pcs, cls = np.zeros(cta, np.int64), np.zeros(cta, np.int64)
+        for j in range(cta):
+            f = oracle.canon_fields(o.get_state(j))
+            pc, mem = int(f["PC"]), f["mem"]
+            pcs[j] = pc
+            cls[j] = -1 if f["halted"] or pc >= 0xFFF else int(mem[pc]) >> 4
+        return pcs, cls
+
+    def tally(name, order, pcs, cls):
+        for w in range(cta // 32):
+            idx = order[32 * w: 32 * w + 32]
+            dp, dc = len(set(pcs[idx].tolist())), len(set(cls[idx].tolist()))
+            sc = score[name]
+            sc["pcs"] += dp
+            sc["cls"] += dc
+            sc["pc_uni"] += dp == 1
+            sc["cls_uni"] += dc == 1
+
+    ident = np.arange(cta)
+    for t in range(warm, warm + steps):
+        a = workloads.gen.actions(workloads.ACTION_SEED, t, cta, na)
+        keys = [0 if x == 0 else 1 << spec["action_keys"][x - 1] for x in a]
+        for _ in range(fs):
+            pcs, cls = peek()
+            frame_order = np.lexsort((cls, pcs))
+            for k in range(ipf):
+                if k:
+                    pcs, cls = peek()
+                tally("identity", ident, pcs, cls)
+                tally("frame", frame_order, pcs, cls)
+                tally("cycle", np.lexsort((cls, pcs)), pcs, cls)
+                wc += cta // 32
+                for j in range(cta):
+                    o.run_cycles(j, 1, keys[j])
+            for j in range(cta):
+                o.tick_timers(j)
+    return {g: {"distinct_pcs": v["pcs"] / wc, "distinct_classes": v["cls"] / wc,
+                "pc_uniform": v["pc_uni"] / wc, "class_uniform": v["cls_uni"] / wc} for g, v in score.items()}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_workload_structure.md"))
     ap.add_argument("--games", nargs="*", default=GAMES)
+    ap.add_argument("--regroup-out", default=None,
+                    help="also write the NEXT-2 regrouping study (regroup()) to this file")
     args = ap.parse_args()
+    if args.regroup_out:
+        rl = ["| game | grouping | distinct PCs / warp-cycle | distinct classes / warp-cycle | "
+              "PC-uniform warp-cycles | class-uniform warp-cycles |", "|---|---|---|---|---|---|"]
+        for g in args.games:
+            r = regroup(g)
+            for name, v in r.items():
+                rl.append(f"| {g} | {name} | {v['distinct_pcs']:.2f} | {v['distinct_classes']:.2f} | "
+                          f"{100 * v['pc_uniform']:.1f}% | {100 * v['class_uniform']:.1f}% |")
+                print(rl[-1], flush=True)
+        with open(args.regroup_out, "w") as f:
+            f.write("# NEXT-2 regrouping study (oracle replay of one 128-env CTA, random actions)\n\n"
+                    "Generated by `python -m tests.tools.workload_structure --regroup-out ...` "
+                    "(`regroup()`): 24 steps after a 300-step warm-up; identity = lane is env (the "
+                    "kernel as built), frame = envs sorted by (PC, class) once per frame and held "
+                    "for its cycles, cycle = re-sorted every cycle (unreachable upper bound).\n\n"
+                    + "\n".join(rl) + "\n")
+        return
     lines = ["| game | top classes (share of instructions) | DXYN/step | rows/DXYN | episodes/1k steps | "
              "distinct PCs per warp-cycle | idle lane-cycles | all-32-idle frame-tail cycles | "
              "warp-cycles by DXYN path (grouped / single-row / lane-parallel / cooperative) |",
