@@ -275,6 +275,42 @@ def time_config(rom, spec, n, steps, warmup, rank_offset, aseed, torch, OctaxEnv
     return total_ms, per, (env, acts, stream)
 
 
+def time_rollout(rom, spec, n, T, reps, warmup_reps, rank_offset, aseed, torch, OctaxEnv, barrier=None,
+                 on_rollout=None):
+    """Fused rollout mode (octax_rollout, SURVEY d.8 mode "fused"): `reps` launches of T steps
+    each, actions generated inside the kernel (the step mode's actions are generated before its
+    timed region, so this mode does strictly more work per step), obs / reward / done written
+    every step into the same [n] buffers as the step mode.  CUDA events on the env's stream;
+    on_rollout(env, stream) after every rollout inside the timed region.  Returns
+    (total_ms, per-rollout ms, env)."""
+    stream = torch.cuda.Stream()
+    env = OctaxEnv(rom, spec, n, 0x0C7A251001764000, env_offset=rank_offset, stream=stream)
+    obs, rew, done = env.obs, env.reward, env.done
+    t = 0
+    with torch.cuda.stream(stream):
+        for _ in range(warmup_reps):
+            env.rollout_into(T, obs, rew, done, aseed=aseed, t0=t)
+            t += T
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+    ev[0].record(stream)
+    with torch.cuda.stream(stream):
+        for k in range(reps):
+            env.rollout_into(T, obs, rew, done, aseed=aseed, t0=t)
+            t += T
+            if on_rollout is not None:
+                on_rollout(env, stream)
+            ev[k + 1].record(stream)
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    per = [ev[k].elapsed_time(ev[k + 1]) for k in range(reps)]
+    return ev[0].elapsed_time(ev[reps]), per, env
+
+
 def issue_model(game, n):
     """ncu instruction counts of the step kernel (profiles/latest_step_full.json), used for the
     ALU-pipe and issue roofs only if the profile is of THIS build and workload: the device-code
@@ -315,6 +351,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fused", action="store_true", help="skip the fused-rollout-mode measurement")
     ap.add_argument("--dist-backend", default="auto", choices=["auto", "nccl", "gloo"],
                     help="auto: nccl with one GPU per rank; gloo when ranks share a device "
                          "(a functional multi-rank run on fewer GPUs than ranks)")
@@ -431,27 +468,32 @@ def main():
         issue = {"achieved": ach_iss, "peak": peak_iss, "unit": "G warp-instr/s", "frac": ach_iss / peak_iss,
                  "warp_instr_per_env_step": im["warp_instr_per_env_step"]}
 
-    # ---- e2e through the host-buffer C-ABI call (H2D actions, D2H obs/reward/done)
+    # ---- e2e through the host-buffer C-ABI calls (H2D actions, D2H results, from / to pinned
+    #      host memory, every step inside the timed region).  Headline: octax_step_host_frame,
+    #      which ships the newest display + reward + done (the host keeps the 3 older displays,
+    #      include/octax.h); "full_obs": octax_step_host shipping the whole 4-plane stack.
     e2e = None
     if not args.no_e2e:
         K = max(3, min(args.steps, 10))
         a_h = torch.empty((K, n), dtype=torch.int32).pin_memory()
         a_h.copy_(acts[:K].cpu())
         o_h = torch.empty((n, env.obs_per_env), dtype=torch.uint8).pin_memory()
+        f_h = torch.empty((n, 32, 8), dtype=torch.uint8).pin_memory()
         r_h = torch.empty(n, dtype=torch.float32).pin_memory()
         d_h = torch.empty(n, dtype=torch.uint8).pin_memory()
         nd = lambda t: t.numpy()
-        env.step_host(nd(a_h[0]), nd(o_h), nd(r_h), nd(d_h))  # warm the staging buffers
-        barrier()
-        t0 = time.perf_counter()
-        for k in range(K):
-            env.step_host(nd(a_h[k]), nd(o_h), nd(r_h), nd(d_h))
-        dt = odist.max_over_ranks(torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda"))
-        e2e = {"value": world * n * K / float(dt.item()), "unit": "env steps/s",
-               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": (env.obs_per_env + 4 + 1) * n,
-               "steps": K, "path": "octax_step_host (pinned host buffers)"}
-        # the e2e roof: this box's pinned D2H copy bandwidth for the same bytes (plain
-        # cudaMemcpyAsync of a device buffer into the pinned obs buffer, best of 3)
+
+        def run(fn, out):
+            fn(nd(a_h[0]), nd(out), nd(r_h), nd(d_h))  # warm the staging buffers
+            barrier()
+            t0 = time.perf_counter()
+            for k in range(K):
+                fn(nd(a_h[k]), nd(out), nd(r_h), nd(d_h))
+            dt = odist.max_over_ranks(torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda"))
+            return world * n * K / float(dt.item())
+
+        # the link roof: this box's pinned D2H copy bandwidth (plain cudaMemcpyAsync of a device
+        # buffer into the pinned obs buffer, best of 3)
         src = torch.empty((n, env.obs_per_env), dtype=torch.uint8, device="cuda")
         best = None
         for _ in range(3):
@@ -462,14 +504,52 @@ def main():
             t = time.perf_counter() - t0
             best = t if best is None else min(best, t)
         d2h_gbs = o_h.numel() / best / 1e9
-        bytes_step = e2e["h2d_bytes_per_step"] + e2e["d2h_bytes_per_step"]
-        roof = d2h_gbs * 1e9 / (bytes_step / n)
-        e2e["link"] = {"d2h_gbs_measured": d2h_gbs, "bytes_per_env_step": bytes_step / n,
-                       "roof_env_steps_per_s": roof * world, "frac": e2e["value"] / (roof * world)}
         del src
+
+        def link(value, bytes_step):
+            roof = d2h_gbs * 1e9 / (bytes_step / n) * world
+            return {"d2h_gbs_measured": d2h_gbs, "bytes_per_env_step": bytes_step / n,
+                    "roof_env_steps_per_s": roof, "frac": value / roof}
+
+        vf = run(env.step_host_frame, f_h)
+        vfull = run(env.step_host, o_h)
+        bf, bfull = (4 + 256 + 4 + 1) * n, (4 + env.obs_per_env + 4 + 1) * n
+        e2e = {"value": vf, "unit": "env steps/s", "h2d_bytes_per_step": 4 * n,
+               "d2h_bytes_per_step": (256 + 4 + 1) * n, "steps": K,
+               "path": "octax_step_host_frame (pinned host buffers; newest display + reward + done, "
+                       "the host keeps the three older displays)",
+               "link": link(vf, bf),
+               "full_obs": {"value": vfull, "h2d_bytes_per_step": 4 * n,
+                            "d2h_bytes_per_step": (env.obs_per_env + 4 + 1) * n,
+                            "path": "octax_step_host (whole 4-plane stack)", "link": link(vfull, bfull)}}
     env.close()
     del acts
     torch.cuda.empty_cache()
+
+    # ---- fused rollout mode at the headline size (SURVEY d.8 mode "fused"): 100-step rollouts
+    #       in one launch each, in-kernel actions, one stats all-reduce per rollout
+    fused = None
+    if not args.no_fused:
+        fst = torch.zeros(4, dtype=torch.int64, device="cuda")
+
+        def on_fused(env_, stream_):
+            with torch.cuda.stream(stream_):
+                env_.stats_device(fst)
+                odist.reduce_stats(fst)
+
+        R = 2
+        tm, per_r, fenv = time_rollout(rom, spec, n, 100, R, 1, offset, workloads.ACTION_SEED, torch, OctaxEnv,
+                                       barrier, on_rollout=on_fused)
+        fenv.close()
+        tf = float(odist.max_over_ranks(torch.tensor([tm], dtype=torch.float64, device="cuda")).item())
+        fv = world * n * 100 * R / (tf / 1e3)
+        fused = {"mode": "fused", "steps_per_rollout": 100, "rollouts_timed": R, "warmup_rollouts": 1,
+                 "steps_per_s": fv, "frames_per_s": 4 * fv, "ms_per_step": tf / (100 * R),
+                 "ms_per_rollout_median": sorted(per_r)[len(per_r) // 2],
+                 "vs_step_mode": fv / value, "stats": [int(x) for x in fst.cpu().tolist()],
+                 "actions": "generated inside the rollout kernel (Philox domain 1, same stream as octax_gen_actions)",
+                 "outputs": "obs / reward / done written every step (same [n] buffers as the step mode)"}
+        torch.cuda.empty_cache()
 
     # ---- sweep of smaller per-GPU env counts (context; parity-test configs): per-launch
     #      and CUDA-graph-captured (launch overhead dominates below ~64K envs)
@@ -489,9 +569,17 @@ def main():
                 row[f"steps_per_s_{key}"] = sps
                 row[f"ms_per_step_{key}"] = tt / ks
             row["frames_per_s_graph"] = 4 * row["steps_per_s_graph"]
+            tm, _, fenv = time_rollout(rom, spec, m, 100, 2, 1, odist.shard(rank, world, m)[0],
+                                       workloads.ACTION_SEED, torch, OctaxEnv, barrier)
+            fenv.close()
+            tt = float(odist.max_over_ranks(torch.tensor([tm], dtype=torch.float64, device="cuda")).item())
+            row["steps_per_s_fused"] = world * m * 200 / (tt / 1e3)
+            row["ms_per_step_fused"] = tt / 200
             sweep.append(row)
         sweep.append({"envs_per_gpu": n, "steps_per_s_launch": value, "frames_per_s_launch": 4 * value,
-                      "ms_per_step_launch": t_max / args.steps})
+                      "ms_per_step_launch": t_max / args.steps,
+                      **({"steps_per_s_fused": fused["steps_per_s"], "ms_per_step_fused": fused["ms_per_step"]}
+                         if fused else {})})
 
     # ---- per-game throughput at BASELINE configs[3]'s size (262,144 envs per GPU): the
     #      paper claims one number for all games; a SIMT interpreter is game dependent
@@ -542,6 +630,7 @@ def main():
                           "peak_source": peak_src}),
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "fused": fused,
             "state_digest": digest,
             "gpu_launches": args.steps,
             "clocks": clk.summary(),

@@ -157,6 +157,9 @@ typedef struct {
   void *final_obs_out;
   int32_t *episode_return_out;
   uint32_t *episode_length_out;
+  void *frame_out;      /* uint8 [n][32][8] packed: this step's newest display (obs plane 3) alone,
+                           contiguous, all envs -- what a consumer keeping its own 3-display
+                           history needs (octax_step_host_frame) */
 } octax_step_extras;
 
 /* octax_step plus the extras above (extras may be NULL = octax_step). */
@@ -171,9 +174,40 @@ octax_status octax_step_host(octax_env *e, const int32_t *actions_host, void *ob
                              float *reward_host, uint8_t *done_host, uint8_t *terminated_host,
                              uint8_t *truncated_host);
 
+/* Host step that ships only what changed (NEXT-3 host variant): like octax_step_host, but the
+ * device->host copy carries the NEWEST display (uint8 [n][32][8] packed, = obs plane 3) instead of
+ * the 4-plane stack -- 261 instead of 1,029 bytes per env.  The caller keeps the three previous
+ * displays: obs = [d(t-3), d(t-2), d(t-1), frame], except that an env with done = 1 was reset in
+ * this step (A10), so its 4 planes all equal the frame.  A host history started from octax_reset's
+ * obs (4 equal planes) reproduces octax_step's obs exactly (tests/test_gpu_parity.py).  Valid for
+ * the default stacking (A3); with OCTAX_OBS_STACK_FRAMES the frame is still the newest display but
+ * the other planes are intermediate frames the host cannot rebuild.  Synchronises the stream. */
+octax_status octax_step_host_frame(octax_env *e, const int32_t *actions_host, void *frame_host,
+                                   float *reward_host, uint8_t *done_host, uint8_t *terminated_host,
+                                   uint8_t *truncated_host);
+
 /* Synthetic benchmark actions (device, int32 [n]):
  * a_j = Philox4x32-10(ctr = {t_lo, t_hi, gid_j, 1}, key = aseed).out0 mod n_actions. */
 octax_status octax_gen_actions(octax_env *e, uint64_t aseed, uint64_t t, int32_t *actions_out);
+
+/* Fused rollout (SURVEY 8(d) d.3 / d.8 mode "fused"; the paper's 100-step rollouts):
+ * T consecutive environment steps of all n envs in ONE kernel launch, the VM state and the
+ * framebuffer kept on chip across the T steps.  Bit-identical to T octax_step calls:
+ *  - step t (0 <= t < T) takes actions[t*n + j] (DEVICE int32 [T][n]) when actions != NULL,
+ *    else the action octax_gen_actions(aseed, t0 + t) would produce, generated in the kernel
+ *    (Philox4x32-10, ctr = {t_lo, t_hi, gid, 1}, key = aseed; SURVEY 2.3 K6 fused into K1);
+ *  - step t's obs goes to (uint8*)obs_out + t*obs_step_stride (bytes, a multiple of 16; 0 =
+ *    every step overwrites the same [n] obs buffer, so the last step's obs remains), its
+ *    reward / done / terminated / truncated to [t*out_step_stride + j] (elements; 0 = same
+ *    buffers every step).  terminated_out / truncated_out may be NULL.  All DEVICE buffers.
+ *  - a non-zero stride must cover all n envs (obs: >= n * 1024 bytes; outputs: >= n).
+ * Same-step auto-reset (A10) runs inline, also for specs with startup segments.  Packed obs
+ * only: a handle created with OCTAX_OBS_BOOL_XMAJOR gets OCTAX_E_INVALID_ARG (either stacking
+ * mode is supported).  T = 0 is a no-op.  Stream-ordered, no host synchronisation; the
+ * statistics count all T steps. */
+octax_status octax_rollout(octax_env *e, uint32_t T, const int32_t *actions, uint64_t aseed, uint64_t t0,
+                           void *obs_out, uint64_t obs_step_stride, float *reward_out, uint8_t *done_out,
+                           uint8_t *terminated_out, uint8_t *truncated_out, uint64_t out_step_stride);
 
 /* Episode statistics since create/reset: {sum of returns of finished episodes,
  * finished episodes, env steps, error flags} (int64).  Synchronises the stream.

@@ -365,6 +365,7 @@ struct octax_env {
   uint8_t *d_obs = nullptr;
   float *d_reward = nullptr;
   uint8_t *d_flags = nullptr;  // done | term | trunc, 3*n
+  uint8_t *d_frame = nullptr;  // [n][256] newest display (octax_step_host_frame)
   // get/set state staging (lazy)
   uint64_t *d_ids = nullptr;
   uint8_t *d_canon = nullptr;
@@ -383,6 +384,7 @@ static void free_env(octax_env *e) {
   cudaFree(e->d_obs);
   cudaFree(e->d_reward);
   cudaFree(e->d_flags);
+  cudaFree(e->d_frame);
   cudaFree(e->d_ids);
   cudaFree(e->d_canon);
   cudaSetDevice(prev);
@@ -535,9 +537,11 @@ extern "C" octax_status octax_step_ex(octax_env *e, const int32_t *actions, void
   uint8_t *packed = e->obs_format == OCTAX_OBS_PACKED ? (uint8_t *)obs_out : e->packed_scratch;
   StepParams p = e->p;
   p.final_obs = nullptr;
+  p.frame_out = nullptr;
   p.ep_ret_out = nullptr;
   p.ep_len_out = nullptr;
   if (extras) {
+    p.frame_out = (uint8_t *)extras->frame_out;
     p.ep_ret_out = extras->episode_return_out;
     p.ep_len_out = extras->episode_length_out;
     if (extras->final_obs_out) {
@@ -582,6 +586,69 @@ extern "C" octax_status octax_step_host(octax_env *e, const int32_t *actions_hos
   octax_status st = octax_step(e, e->d_actions, e->d_obs, e->d_reward, e->d_flags, e->d_flags + n, e->d_flags + 2 * n);
   if (st != OCTAX_OK) return st;
   CU(cudaMemcpyAsync(obs_host, e->d_obs, (size_t)e->obs_bytes * n, cudaMemcpyDeviceToHost, e->stream), "D2H obs");
+  CU(cudaMemcpyAsync(reward_host, e->d_reward, 4 * n, cudaMemcpyDeviceToHost, e->stream), "D2H reward");
+  CU(cudaMemcpyAsync(done_host, e->d_flags, n, cudaMemcpyDeviceToHost, e->stream), "D2H done");
+  if (terminated_host)
+    CU(cudaMemcpyAsync(terminated_host, e->d_flags + n, n, cudaMemcpyDeviceToHost, e->stream), "D2H term");
+  if (truncated_host)
+    CU(cudaMemcpyAsync(truncated_host, e->d_flags + 2 * n, n, cudaMemcpyDeviceToHost, e->stream), "D2H trunc");
+  CU(cudaStreamSynchronize(e->stream), "sync");
+  return OCTAX_OK;
+}
+
+extern "C" octax_status octax_rollout(octax_env *e, uint32_t T, const int32_t *actions, uint64_t aseed, uint64_t t0,
+                                      void *obs_out, uint64_t obs_step_stride, float *reward_out, uint8_t *done_out,
+                                      uint8_t *terminated_out, uint8_t *truncated_out, uint64_t out_step_stride) {
+  if (!e || !obs_out || !reward_out || !done_out)
+    return set_err(OCTAX_E_INVALID_ARG, "NULL argument to octax_rollout");
+  if (T == 0) return OCTAX_OK;
+  if (e->obs_format != OCTAX_OBS_PACKED)
+    return set_err(OCTAX_E_INVALID_ARG, "octax_rollout: packed observations only (obs_format OCTAX_OBS_PACKED)");
+  if (obs_step_stride % 16 != 0)
+    return set_err(OCTAX_E_INVALID_ARG, "octax_rollout: obs_step_stride must be a multiple of 16 bytes");
+  if ((obs_step_stride != 0 && obs_step_stride < (uint64_t)e->obs_bytes * e->n) ||
+      (out_step_stride != 0 && out_step_stride < e->n))
+    return set_err(OCTAX_E_INVALID_ARG, "octax_rollout: a non-zero step stride must cover all n envs");
+  DeviceGuard g(e->device);
+  StepParams p = e->p;
+  p.final_obs = nullptr;
+  p.frame_out = nullptr;
+  p.ep_ret_out = nullptr;
+  p.ep_len_out = nullptr;
+  p.reset_ids = nullptr;  // resets run inline inside the rollout kernel
+  p.reset_count = nullptr;
+  p.T = T;
+  p.aseed = aseed;
+  p.t0 = t0;
+  p.obs_stride = obs_step_stride / 8;
+  p.out_stride = out_step_stride;
+  CU(launch_step(p, MODE_ROLLOUT, actions, (uint8_t *)obs_out, reward_out, done_out, terminated_out, truncated_out,
+                 e->stream),
+     "rollout kernel");
+  e->p.head = (e->p.head + T) & 3u;
+  return OCTAX_OK;
+}
+
+extern "C" octax_status octax_step_host_frame(octax_env *e, const int32_t *actions_host, void *frame_host,
+                                              float *reward_host, uint8_t *done_host, uint8_t *terminated_host,
+                                              uint8_t *truncated_host) {
+  if (!e || !actions_host || !frame_host || !reward_host || !done_host)
+    return set_err(OCTAX_E_INVALID_ARG, "NULL argument to octax_step_host_frame");
+  DeviceGuard g(e->device);
+  const uint64_t n = e->n;
+  if (!e->d_actions) {
+    CU(cudaMalloc(&e->d_actions, 4 * n), "cudaMalloc");
+    CU(cudaMalloc(&e->d_obs, (size_t)e->obs_bytes * n), "cudaMalloc");
+    CU(cudaMalloc(&e->d_reward, 4 * n), "cudaMalloc");
+    CU(cudaMalloc(&e->d_flags, 3 * n), "cudaMalloc");
+  }
+  if (!e->d_frame) CU(cudaMalloc(&e->d_frame, 256 * n), "cudaMalloc(frame)");
+  CU(cudaMemcpyAsync(e->d_actions, actions_host, 4 * n, cudaMemcpyHostToDevice, e->stream), "H2D actions");
+  octax_step_extras ex = {nullptr, nullptr, nullptr, e->d_frame};
+  octax_status st = octax_step_ex(e, e->d_actions, e->d_obs, e->d_reward, e->d_flags, e->d_flags + n,
+                                  e->d_flags + 2 * n, &ex);
+  if (st != OCTAX_OK) return st;
+  CU(cudaMemcpyAsync(frame_host, e->d_frame, 256 * n, cudaMemcpyDeviceToHost, e->stream), "D2H frame");
   CU(cudaMemcpyAsync(reward_host, e->d_reward, 4 * n, cudaMemcpyDeviceToHost, e->stream), "D2H reward");
   CU(cudaMemcpyAsync(done_host, e->d_flags, n, cudaMemcpyDeviceToHost, e->stream), "D2H done");
   if (terminated_host)

@@ -146,6 +146,7 @@ struct StepParams {
   DevState s;
   // optional per-step extra outputs (octax_step_ex), nullptr when not requested
   uint8_t *final_obs;      // packed [n][4][32][8]: obs of the terminal transition, done envs only
+  uint8_t *frame_out;      // packed [n][32][8]: this step's newest display (obs plane 3), all envs
   int32_t *ep_ret_out;     // return of the episode that ended this step (0 if none)
   uint32_t *ep_len_out;    // its length in steps (0 if none)
   uint32_t *reset_count;   // deferred resets (specs with startup segments): [1] counter and
@@ -162,6 +163,14 @@ struct StepParams {
   uint32_t stack_frames;  // OCTAX_OBS_STACK_FRAMES: obs = last 4 frames of the step
   uint32_t n_actions;     // n_action_keys + 1
   uint32_t n_startup;
+  // fused rollout (MODE_ROLLOUT, octax_rollout): T steps per launch; step t's obs at obs + t *
+  // obs_stride (u64 units), reward / done / terminated / truncated at [t * out_stride + env];
+  // actions [T][n] if given, else generated in-kernel for step index t0 + t with key aseed
+  uint32_t T;
+  uint64_t aseed;
+  uint64_t t0;
+  uint64_t obs_stride;
+  uint64_t out_stride;
   uint16_t keymask[17];   // action -> key mask
   uint16_t pad0;
   uint32_t startup_keys[kMaxStartup];
@@ -170,6 +179,6 @@ struct StepParams {
   Program term;
 };
 
-enum Mode : int { MODE_STEP = 0, MODE_RESET = 1 };
+enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_ROLLOUT = 2 };
 
 }  // namespace octax

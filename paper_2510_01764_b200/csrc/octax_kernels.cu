@@ -78,6 +78,9 @@ struct __align__(128) Smem {
 
 size_t smem_bytes() { return sizeof(Smem); }
 
+// byte `a` of the CTA's shared-memory copy of the pristine image (zeros, font, ROM)
+#define IMG(a) ((uint32_t)sm.img[a])
+
 // framebuffer row `r` of CTA-local env `e`: XOR swizzle on the low 4 row bits
 __device__ __forceinline__ uint32_t fb_idx(uint32_t e, uint32_t r) {
   OCTAX_CHECK(e < (uint32_t)kBlock && r < 32u);
@@ -108,12 +111,12 @@ __device__ __forceinline__ uint32_t philox_out0(uint32_t c0, uint32_t c1, uint32
 // 32 KB framebuffer block of ring slot `h` into shared memory on one mbarrier.
 __device__ __forceinline__ void stage_issue(Smem &sm, const uint8_t *img, const uint64_t *fb_src) {
   uint32_t bar = (uint32_t)__cvta_generic_to_shared(&sm.bar);
-  uint32_t dst = (uint32_t)__cvta_generic_to_shared(sm.img);
   const uint32_t bytes = kStageBytes + (fb_src ? (uint32_t)sizeof(sm.fb) : 0u);
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(sm.img);
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
       "l"(img), "r"(kStageBytes), "r"(bar)
@@ -171,6 +174,12 @@ __device__ __forceinline__ void put_rows(uint64_t *ob_env, uint32_t pl, uint32_t
 // l2 ^ (s & 1) ^ 1 instead and writes rows (l2 ^ s) & ~1 onwards in order.
 __device__ __forceinline__ void put_pair(const uint64_t *fb_env, uint64_t *ob_env, uint32_t pl, uint32_t l2,
                                          uint32_t s) {
+  if ((kSwz & 1u) == 0u) {  // even swizzle: positions l2, l2+1 are one 16-B chunk (one LDS.128,
+                            // conflict free; two 8-B loads were 2-way conflicted)
+    __stcs(reinterpret_cast<ulonglong2 *>(ob_env + pl * 32u + (l2 ^ s)),
+           *reinterpret_cast<const ulonglong2 *>(fb_env + l2));
+    return;
+  }
   const uint32_t hh = s & 1u;
   const uint64_t lo = fb_env[l2 ^ hh], hi = fb_env[l2 ^ hh ^ 1u];
   __stcs(reinterpret_cast<ulonglong2 *>(ob_env + pl * 32u + ((l2 ^ s) & ~1u)), make_ulonglong2(lo, hi));
@@ -212,12 +221,12 @@ constexpr uint32_t kPad = 1u << 24;
 #define HAS(d, F) (((d) & ((F) | kPad)) != 0u)
 
 
-__device__ __forceinline__ uint32_t rd(const Smem &sm, const Lane &L, uint32_t a) {
+__device__ __forceinline__ uint32_t rd(const Smem &sm, const StepParams &p, const Lane &L, uint32_t a) {
   OCTAX_CHECK(a < 4096u);
-  return ((L.dirty >> (a >> 6)) & 1ull) ? (uint32_t)L.ram[a] : (uint32_t)sm.img[a];
+  return ((L.dirty >> (a >> 6)) & 1ull) ? (uint32_t)L.ram[a] : IMG(a);
 }
 
-__device__ __forceinline__ void wr(const Smem &sm, Lane &L, uint32_t a, uint32_t v) {
+__device__ __forceinline__ void wr(const Smem &sm, const StepParams &p, Lane &L, uint32_t a, uint32_t v) {
   OCTAX_CHECK(a < 4096u);
   uint32_t b = a >> 6;
   if (!((L.dirty >> b) & 1ull)) {  // copy-on-write: materialise the 64-B block
@@ -241,6 +250,16 @@ __device__ __forceinline__ void power_on(Smem &sm, Lane &L, const StepParams &p,
   L.dirty = 0;
   L.dec = __ldg(p.s.dec + 0x200);
   L.stk_dirty = 1;
+}
+
+// shared-memory stack -> the env's 32-B HBM stack row
+__device__ __forceinline__ void store_stack(const Smem &sm, const StepParams &p, int tid, uint64_t env) {
+  uint32_t sw[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    sw[k] = (uint32_t)sm.stk[(2 * k) * kBlock + tid] | ((uint32_t)sm.stk[(2 * k + 1) * kBlock + tid] << 16);
+  p.s.stack[env * 2] = make_uint4(sw[0], sw[1], sw[2], sw[3]);
+  p.s.stack[env * 2 + 1] = make_uint4(sw[4], sw[5], sw[6], sw[7]);
 }
 
 // Cooperative DXYN for every lane with do_draw (must be called by all 32 lanes).
@@ -295,7 +314,7 @@ __device__ __noinline__ void draw_coop(Smem &sm, const Lane &L, const StepParams
       const uint32_t xj = pj & 63u, yy = (((pj >> 6) & 31u) + r) & 31u, a = (pj >> 11) + r;
       uint32_t byte = 0;
       if (a <= 0xFFFu)
-        byte = ((dj >> (a >> 6)) & 1ull) ? (uint32_t)rj[a] : (uint32_t)sm.img[a];
+        byte = ((dj >> (a >> 6)) & 1ull) ? (uint32_t)rj[a] : IMG(a);
       uint64_t m = (uint64_t)byte << 56;
       m = bswap64(wrap ? ((m >> xj) | (xj ? (m << (64u - xj)) : 0ull)) : (m >> xj));
       uint64_t *row = &sm.fb[fb_idx(wl + j, yy)];
@@ -323,6 +342,10 @@ __device__ __forceinline__ void draw_lanes(Smem &sm, Lane &L, const StepParams &
   if (wdirty) slowb |= do_draw & (((L.dirty >> (base >> 6)) & 3ull) != 0ull);
   const uint32_t sh = x0 & 7u, q8 = (x0 >> 3) * 8u, swz = (uint32_t)tid & kSwz;
   uint64_t *rows = &sm.fb[(uint32_t)tid * 32u];
+  // lanes without rows XOR a zero mask into rows of their own env; start them at row tid & 0x11,
+  // which puts the 16 lanes of each half-warp on 16 distinct bank pairs for every r < 8 (instead
+  // of wherever their VY points), so only the drawing lanes can bank-conflict
+  y0 = nrows != 0u ? y0 : ((uint32_t)tid & 0x11u);
   uint64_t hit = 0;
   if (!wrap && !__any_sync(kFull, slowb)) {
     // sprite bytes base..base+7 realigned from three 32-bit image words
@@ -344,7 +367,7 @@ __device__ __forceinline__ void draw_lanes(Smem &sm, Lane &L, const StepParams &
   } else {
     for (uint32_t r = 0; r < maxr; ++r) {
       const uint32_t a = base + r;
-      uint32_t byte = (r < nrows && a <= 0xFFFu) ? rd(sm, L, a) : 0u;
+      uint32_t byte = (r < nrows && a <= 0xFFFu) ? rd(sm, p, L, a) : 0u;
       const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> sh, 0, 0x4401);
       const uint64_t m = wrap ? ((w << q8) | (q8 ? (w >> (64u - q8)) : 0ull)) : (w << q8);
       uint64_t *row = rows + (((y0 + r) & 31u) ^ swz);
@@ -390,9 +413,9 @@ __device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepP
     uint32_t byte = 0;
     if (DIRTY) {
       if (a <= 0xFFFu)
-        byte = ((od >> (a >> 6)) & 1ull) ? (uint32_t)oram[a] : (uint32_t)sm.img[a];
+        byte = ((od >> (a >> 6)) & 1ull) ? (uint32_t)oram[a] : IMG(a);
     } else {
-      byte = a <= 0xFFFu ? (uint32_t)sm.img[a] : 0u;  // no global load on the common path
+      byte = a <= 0xFFFu ? IMG(a) : 0u;  // no HBM-backed RAM load on the common path
     }
     const uint32_t yy = (((q >> 6) & 31u) + r) & 31u, q8 = ox & 0x38u;
     const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> (ox & 7u), 0, 0x4401);
@@ -410,13 +433,13 @@ __device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepP
 // DXYN when no lane of the warp draws more than one row (a 1-row sprite, or clipped at
 // the bottom): one row step, no sprite-word realignment.
 template <bool DIRTY>
-__device__ __forceinline__ void draw_one(Smem &sm, const Lane &L, int tid, bool draws, uint32_t x0, uint32_t y0,
+__device__ __forceinline__ void draw_one(Smem &sm, const StepParams &p, const Lane &L, int tid, bool draws, uint32_t x0, uint32_t y0,
                                          uint32_t base, uint32_t quirks, bool vfw) {
   bool hit = false;
   if (draws) {
     uint32_t byte;
-    if (DIRTY) byte = rd(sm, L, base);
-    else byte = sm.img[base];
+    if (DIRTY) byte = rd(sm, p, L, base);
+    else byte = IMG(base);
     const uint32_t q8 = x0 & 0x38u;
     const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> (x0 & 7u), 0, 0x4401);
     const uint64_t mk = (quirks & 8u) ? ((w << q8) | (q8 ? (w >> (64u - q8)) : 0ull)) : (w << q8);
@@ -446,7 +469,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   if (wdirty) {
     const bool slow = act & (pc <= 0xFFEu) & (((L.dirty >> (pc >> 6)) & 3ull) != 0ull);
     if (__any_sync(kFull, slow)) {
-      if (slow) make_entry((rd(sm, L, pc) << 8) | rd(sm, L, pc + 1), sm.dtab, quirks, e.x, e.y);
+      if (slow) make_entry((rd(sm, p, L, pc) << 8) | rd(sm, p, L, pc + 1), sm.dtab, quirks, e.x, e.y);
     }
   }
   const uint32_t d = e.x, nnn = e.y >> 20, nn = nnn & 255u, n = nnn & 15u, x = nnn >> 8;
@@ -545,14 +568,14 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   if (__any_sync(kFull, do_mem)) {
     if (do_mem) {
       if (f33) {
-        wr(sm, L, L.I & 0xFFFu, vx / 100u);
-        wr(sm, L, (L.I + 1u) & 0xFFFu, (vx / 10u) % 10u);
-        wr(sm, L, (L.I + 2u) & 0xFFFu, vx % 10u);
+        wr(sm, p, L, L.I & 0xFFFu, vx / 100u);
+        wr(sm, p, L, (L.I + 1u) & 0xFFFu, (vx / 10u) % 10u);
+        wr(sm, p, L, (L.I + 2u) & 0xFFFu, vx % 10u);
       } else {
         if (f55) {
-          for (uint32_t k = 0; k <= x; ++k) wr(sm, L, (L.I + k) & 0xFFFu, VREG(k));
+          for (uint32_t k = 0; k <= x; ++k) wr(sm, p, L, (L.I + k) & 0xFFFu, VREG(k));
         } else {
-          for (uint32_t k = 0; k <= x; ++k) VREG(k) = (uint8_t)rd(sm, L, (L.I + k) & 0xFFFu);
+          for (uint32_t k = 0; k <= x; ++k) VREG(k) = (uint8_t)rd(sm, p, L, (L.I + k) & 0xFFFu);
         }
         if (quirks & 2u) L.I = (L.I + x + 1u) & 0xFFFFu;
       }
@@ -576,8 +599,8 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
         draw_groups<false, SCAT>(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
     }
     else if (maxr == 1u) {
-      if (wdirty) draw_one<true>(sm, L, tid, nrows != 0u, vx & 63u, y0, L.I & 0xFFFu, quirks, do_draw);
-      else draw_one<false>(sm, L, tid, nrows != 0u, vx & 63u, y0, L.I & 0xFFFu, quirks, do_draw);
+      if (wdirty) draw_one<true>(sm, p, L, tid, nrows != 0u, vx & 63u, y0, L.I & 0xFFFu, quirks, do_draw);
+      else draw_one<false>(sm, p, L, tid, nrows != 0u, vx & 63u, y0, L.I & 0xFFFu, quirks, do_draw);
     } else if (maxr <= kLaneDrawMax)
       draw_lanes(sm, L, p, tid, do_draw, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
     else
@@ -604,7 +627,7 @@ __device__ __forceinline__ void run_frames(Smem &sm, Lane &L, const StepParams &
 // Postfix bytecode evaluator (uniform control flow: every lane runs the same
 // program).  The stack lives in registers as a shift register with compile-time
 // slots (depth <= kMaxDepth is enforced at create), so it costs no shared memory.
-__device__ __forceinline__ uint32_t eval(const Program &P, Smem &sm, const Lane &L, int tid) {
+__device__ __forceinline__ uint32_t eval(const Program &P, Smem &sm, const StepParams &p, const Lane &L, int tid) {
   uint32_t st[kMaxDepth];
 #pragma unroll
   for (int k = 0; k < kMaxDepth; ++k) st[k] = 0;
@@ -620,7 +643,7 @@ __device__ __forceinline__ uint32_t eval(const Program &P, Smem &sm, const Lane 
       st[0] = v;
     } else if (in.op < X_MUL) {  // unary on the top
       const uint32_t t = st[0];
-      st[0] = in.op == X_MEM ? rd(sm, L, t & 0xFFFu) : in.op == X_NEG ? 0u - t : in.op == X_NOT ? (uint32_t)(t == 0u) : ~t;
+      st[0] = in.op == X_MEM ? rd(sm, p, L, t & 0xFFFu) : in.op == X_NEG ? 0u - t : in.op == X_NOT ? (uint32_t)(t == 0u) : ~t;
     } else {  // binary: a = second, b = top
       const uint32_t a = st[1], b = st[0];
       uint32_t r;
@@ -671,16 +694,13 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   const uint32_t nlive = p.n - block0 < (uint64_t)kBlock ? (uint32_t)(p.n - block0) : (uint32_t)kBlock;
   const bool active = (uint32_t)tid < nlive;  // (32-bit: cheap to rematerialise)
   const uint64_t wbase = block0 + (uint64_t)warp * 32;
-  const uint32_t h = p.head;
-  OCTAX_CHECK(h < 4u && blockDim.x == (unsigned)kBlock);
-  uint64_t *__restrict__ obs64 = reinterpret_cast<uint64_t *>(obs);
+  OCTAX_CHECK(p.head < 4u && blockDim.x == (unsigned)kBlock);
   const int ne = p.n > wbase ? (int)((p.n - wbase) < 32 ? (p.n - wbase) : 32) : 0;
-  const uint32_t s0 = (h + 2) & 3, s1 = (h + 3) & 3, s2 = h & 3;
   const uint32_t hh = (uint32_t)lane >> 4, l2 = 2u * ((uint32_t)lane & 15u);  // 16-B chunk lanes
 
   // ---- prologue: TMA bulk copies of the image and (step) the CTA's 32 KB framebuffer
   //      block of ring slot h -- the ring keeps the smem swizzle, so no per-lane work
-  if (tid == 0) stage_issue(sm, p.s.image, MODE == MODE_STEP ? ring_at(p, s2, block0) : nullptr);
+  if (tid == 0) stage_issue(sm, p.s.image, MODE != MODE_RESET ? ring_at(p, p.head & 3u, block0) : nullptr);
 
   Lane L;
   // lanes past n and lanes halted on entry fetch from the E_BAD half of the decode table
@@ -717,11 +737,29 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   stage_wait(sm);
   bool wdirty = __any_sync(kFull, L.dirty != 0ull);  // any lane with private RAM blocks
 
-  uint32_t done = 0, term = 0, trunc = 0, finished = 0, err = 0;
-  float rew = 0.f;
+  // statistics accumulated over the launch's steps (one step, or T in a fused rollout)
+  uint32_t finished = 0, err = 0;
   long long ret_acc = 0;
+  // MODE_ROLLOUT (fused rollout, SURVEY d.3/d.8 "fused", K6 fused into K1): T steps in this
+  // launch with the VM state in registers / shared memory and the framebuffer in shared memory
+  // throughout; each step's display goes to the ring with plain per-warp stores, so after the
+  // prologue a warp needs no CTA barrier until the statistics at the end.
+  const uint32_t T = MODE == MODE_ROLLOUT ? p.T : 1u;
+  for (uint32_t t = 0; t < T; ++t) {
+  const uint32_t h = (p.head + t) & 3u;
+  const uint32_t s0 = (h + 2) & 3, s1 = (h + 3) & 3, s2 = h;
+  uint64_t *__restrict__ obs64 = reinterpret_cast<uint64_t *>(obs) + (MODE == MODE_ROLLOUT ? t * p.obs_stride : 0u);
+  const uint64_t oo = MODE == MODE_ROLLOUT ? t * p.out_stride : 0u;  // step t's reward / done row
+  if (MODE == MODE_ROLLOUT && active) {  // step t's action: given [T][n], or the K6 generator in-kernel
+    const uint64_t ts = p.t0 + t;
+    act_in = actions ? actions[t * p.n + env]
+                     : (int32_t)(philox_out0((uint32_t)ts, (uint32_t)(ts >> 32), gid, 1u, (uint32_t)p.aseed,
+                                             (uint32_t)(p.aseed >> 32)) % p.n_actions);
+  }
+  uint32_t done = 0, term = 0, trunc = 0;
+  float rew = 0.f;
   bool resetting;
-  if (MODE == MODE_STEP) {
+  if (MODE != MODE_RESET) {
     // Stacking (A3): by default obs = the last 4 step-END displays -- planes 0,1 come from
     // the ring (copied one env per VM cycle: loads before the cycle, stores after it, so
     // the HBM latency hides behind it), plane 2 = the step-start display.  With
@@ -770,12 +808,12 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
         // +3% pong, +6..7% brix / Target Shooter; one or three cycles ahead are slower)
         if (cur + 2 < ne) asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + 32));
         cycle<Q0, false>(sm, L, p, tid, lane, block0, gid, active, wdirty);
-        if (cp) {
-          put_rows(opl, 0u, l2 ^ ((uint32_t)cur & kSwz), q);
-          ++cur;
-          rp += 16;
-          opl += 128;
-        }
+        // unconditional bookkeeping: the guarded store is one predicated STG, no branch region
+        // (A/B v34: +0.3..0.7% brix / Target Shooter); `cur` runs past ne, the tail loop is then empty
+        if (cp) put_rows(opl, 0u, l2 ^ ((uint32_t)cur & kSwz), q);
+        ++cur;
+        rp += 16;
+        opl += 128;
       }
       if (L.run) {
         L.dt -= (L.dt != 0u);
@@ -788,24 +826,26 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
           obs64[(wbase + e) * 128 + pl * 32 + lane] = sm.fb[fb_idx(warp * 32 + e, lane)];
       }
     }
+    // envs the per-cycle copy did not reach (fewer than 32 cycles per step): rp / opl already point
+    // at env `cur`, so the ring / obs bases need not stay live through the frame loop
 #pragma unroll 4
-    for (int e = cur; e < ne; ++e) put_rows(odst + e * 128, 0u, l2 ^ ((uint32_t)e & kSwz), __ldcs(rsrc + e * 16));
+    for (int e = cur; e < ne; ++e, rp += 16, opl += 128) put_rows(opl, 0u, l2 ^ ((uint32_t)e & kSwz), __ldcs(rp));
     if (active) L.halted = !L.run;
     if (active) {
-      const uint32_t s = eval(p.score, sm, L, tid);
+      const uint32_t s = eval(p.score, sm, p, L, tid);
       const int32_t d = (int32_t)(s - prev);
       rew = (float)d;
       prev = s;
       ep_ret = (int32_t)((uint32_t)ep_ret + (uint32_t)d);
       steps++;
-      term = (eval(p.term, sm, L, tid) != 0u) || L.halted;
+      term = (eval(p.term, sm, p, L, tid) != 0u) || L.halted;
       trunc = p.max_steps && steps >= p.max_steps;
       done = term | trunc;
-      if (done) { ret_acc = ep_ret; finished = 1; L.episode++; }
-      reward[env] = rew;
-      done_out[env] = (uint8_t)done;
-      if (term_out) term_out[env] = (uint8_t)term;
-      if (trunc_out) trunc_out[env] = (uint8_t)trunc;
+      if (done) { ret_acc += ep_ret; finished++; L.episode++; }
+      reward[oo + env] = rew;
+      done_out[oo + env] = (uint8_t)done;
+      if (term_out) term_out[oo + env] = (uint8_t)term;
+      if (trunc_out) trunc_out[oo + env] = (uint8_t)trunc;
     }
     resetting = active && done;
     // ---- optional extras: the terminal transition's obs and the finished episode's return/length
@@ -863,24 +903,34 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       // its stored PC is the word after it, as the fetch advanced it (a2, A17, A33), except
       // for a fetch past 0xFFE (stored unchanged)
       if (L.halted && L.pc <= 0xFFEu) L.pc += 2u;
+      // ... and, like a lane loaded halted, it then fetches from the E_BAD half of the decode table
+      // (PC bit 16; stored PCs drop it), so a fused rollout's next step runs it without effect
+      if (L.halted) {
+        L.pc |= 0x10000u;
+        L.dec = __ldg(p.s.dec + L.pc);
+      }
       steps = 0;
-      prev = eval(p.score, sm, L, tid);
+      prev = eval(p.score, sm, p, L, tid);
       ep_ret = 0;
     }
   }
   __syncwarp();
 
   // ---- epilogue: the CTA's framebuffer block -> ring slot h+1 with one TMA bulk store
-  //      (all 4 slots on a reset launch); obs plane 3 in row order (all planes on reset)
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
-  __syncthreads();
-  if (tid == 0) {
-    if (MODE == MODE_STEP) {
-      fb_store_issue(sm, ring_at(p, (h + 1) & 3, block0));
-    } else {
-      for (uint32_t sl = 0; sl < 4; ++sl) fb_store_issue(sm, ring_at(p, sl, block0));
+  //      (all 4 slots on a reset launch); obs plane 3 in row order (all planes on reset).
+  //      A fused rollout stores each warp's 32 displays to slot h+1 itself (16-B chunks in
+  //      position order, next to the plane-3 rows) and continues without a CTA barrier.
+  if (MODE != MODE_ROLLOUT) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
+    __syncthreads();
+    if (tid == 0) {
+      if (MODE == MODE_STEP) {
+        fb_store_issue(sm, ring_at(p, (h + 1) & 3, block0));
+      } else {
+        for (uint32_t sl = 0; sl < 4; ++sl) fb_store_issue(sm, ring_at(p, sl, block0));
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   }
   if (obs64) {
     for (int e = 0; e < ne; e += 2)
@@ -889,14 +939,19 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
         const uint64_t *fe = &sm.fb[el * 32u];
         uint64_t *ob = obs64 + (wbase + e + hh) * 128;
         put_pair(fe, ob, 3u, l2, sw);
-        if (MODE != MODE_STEP || ((reset_mask >> (e + hh)) & 1u)) {
+        if (MODE == MODE_STEP && p.frame_out)  // the newest display alone, contiguous (host frame path)
+          put_pair(fe, reinterpret_cast<uint64_t *>(p.frame_out) + (wbase + e + hh) * 32, 0u, l2, sw);
+        if (MODE == MODE_ROLLOUT)  // ring slot h+1: the 16-B chunk at positions l2, l2+1
+          *reinterpret_cast<ulonglong2 *>(ring_at(p, (h + 1) & 3, wbase + e + hh) + l2) =
+              make_ulonglong2(fe[l2], fe[l2 + 1]);
+        if (MODE == MODE_RESET || ((reset_mask >> (e + hh)) & 1u)) {
           put_pair(fe, ob, 0u, l2, sw);
           put_pair(fe, ob, 1u, l2, sw);
           put_pair(fe, ob, 2u, l2, sw);
         }
       }
   }
-  if (MODE == MODE_STEP) {  // reset envs: the other three ring slots hold the reset display too
+  if (MODE != MODE_RESET) {  // reset envs: the other three ring slots hold the reset display too
     uint32_t rm = reset_mask;
     while (rm) {
       const int e = __ffs(rm) - 1;
@@ -908,6 +963,9 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     }
   }
 
+  if (MODE == MODE_ROLLOUT) __syncwarp();  // this step's ring / smem stores before the next step's reads
+  }  // step loop
+
   // ---- store lane state
   if (active) {
     uint32_t w[4] = {0, 0, 0, 0};
@@ -917,20 +975,13 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     p.s.ctrl[env] = make_uint4((L.pc & 0xFFFFu) | (L.I << 16), L.sp | (L.dt << 8) | (L.st << 16) | (L.halted << 24),
                                L.draw, L.episode);
     p.s.book[env] = make_uint4(steps, prev, (uint32_t)ep_ret, 0u);
-    if (L.stk_dirty) {
-      uint32_t sw[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        sw[k] = (uint32_t)sm.stk[(2 * k) * kBlock + tid] | ((uint32_t)sm.stk[(2 * k + 1) * kBlock + tid] << 16);
-      p.s.stack[env * 2] = make_uint4(sw[0], sw[1], sw[2], sw[3]);
-      p.s.stack[env * 2 + 1] = make_uint4(sw[4], sw[5], sw[6], sw[7]);
-    }
+    if (L.stk_dirty) store_stack(sm, p, tid, env);
     p.s.dirty[env] = L.dirty;
   }
 
   // ---- integer episode statistics (a12): warp reduce, CTA reduce, 4 atomics per CTA
-  if (MODE == MODE_STEP) {
-    unsigned long long r = (unsigned long long)ret_acc, f = finished, st = active ? 1u : 0u, er = err;
+  if (MODE != MODE_RESET) {
+    unsigned long long r = (unsigned long long)ret_acc, f = finished, st = active ? T : 0u, er = err;
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       r += __shfl_xor_sync(kFull, r, o);
@@ -948,7 +999,9 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
         else atomicAdd(&p.s.stats[tid], acc);
       }
     }
-  }  if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem outlives the store
+  }
+  if (MODE != MODE_ROLLOUT && tid == 0)
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem outlives the store
 }
 
 // ---------------------------------------------------------------- deferred resets (K3)
@@ -991,7 +1044,7 @@ reset_kernel(const __grid_constant__ StepParams p, uint8_t *__restrict__ obs) {
     if (part) {
       set_keys(L, 0u);
       if (L.halted && L.pc <= 0xFFEu) L.pc += 2u;  // faulted in startup: PC after the fetch (A33)
-      prev = eval(p.score, sm, L, tid);
+      prev = eval(p.score, sm, p, L, tid);
     }
     __syncwarp();
     // the reset display -> obs planes 0..3 and ring slots 0..3, one env per pass, lane = row
@@ -1019,12 +1072,7 @@ reset_kernel(const __grid_constant__ StepParams p, uint8_t *__restrict__ obs) {
       p.s.ctrl[env] = make_uint4((L.pc & 0xFFFFu) | (L.I << 16), L.sp | (L.dt << 8) | (L.st << 16) | (L.halted << 24),
                                  L.draw, L.episode);
       p.s.book[env] = make_uint4(0u, prev, 0u, 0u);
-      uint32_t sw[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        sw[k] = (uint32_t)sm.stk[(2 * k) * kBlock + tid] | ((uint32_t)sm.stk[(2 * k + 1) * kBlock + tid] << 16);
-      p.s.stack[env * 2] = make_uint4(sw[0], sw[1], sw[2], sw[3]);
-      p.s.stack[env * 2 + 1] = make_uint4(sw[4], sw[5], sw[6], sw[7]);
+      store_stack(sm, p, tid, env);
       p.s.dirty[env] = L.dirty;
     }
     __syncwarp();
@@ -1206,6 +1254,9 @@ cudaError_t launch_step(const StepParams &p, int mode, const int32_t *actions, u
     if (e != cudaSuccess || !p.reset_ids) return e;
     return q0 ? launch_resets<true>(p, obs, stream) : launch_resets<false>(p, obs, stream);
   }
+  if (mode == MODE_ROLLOUT)  // inline resets (p.reset_ids == nullptr): no reset_kernel inside a rollout
+    return q0 ? launch_variant<MODE_ROLLOUT, true>(p, actions, obs, reward, done, term, trunc, stream)
+              : launch_variant<MODE_ROLLOUT, false>(p, actions, obs, reward, done, term, trunc, stream);
   return q0 ? launch_variant<MODE_RESET, true>(p, nullptr, obs, nullptr, nullptr, nullptr, nullptr, stream)
             : launch_variant<MODE_RESET, false>(p, nullptr, obs, nullptr, nullptr, nullptr, nullptr, stream);
 }

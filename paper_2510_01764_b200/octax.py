@@ -24,7 +24,7 @@ OBS_STACK_FRAMES = 16
 
 # every symbol include/octax.h declares
 SYMBOLS = (
-    "octax_create", "octax_reset", "octax_step", "octax_step_ex", "octax_step_host", "octax_gen_actions",
+    "octax_create", "octax_reset", "octax_step", "octax_step_ex", "octax_step_host", "octax_step_host_frame", "octax_rollout", "octax_gen_actions",
     "octax_stats", "octax_stats_device", "octax_get_state", "octax_get_states",
     "octax_set_state", "octax_state_digests", "octax_info", "octax_destroy", "octax_last_error",
 )
@@ -59,7 +59,7 @@ class _Spec(ctypes.Structure):
 
 class _Extras(ctypes.Structure):
     _fields_ = [("final_obs_out", ctypes.c_void_p), ("episode_return_out", ctypes.c_void_p),
-                ("episode_length_out", ctypes.c_void_p)]
+                ("episode_length_out", ctypes.c_void_p), ("frame_out", ctypes.c_void_p)]
 
 
 class _Opts(ctypes.Structure):
@@ -85,7 +85,9 @@ def load_library():
     L.octax_step.argtypes = [P, P, P, P, P, P, P]
     L.octax_step_ex.argtypes = [P, P, P, P, P, P, P, ctypes.POINTER(_Extras)]
     L.octax_step_host.argtypes = [P, P, P, P, P, P, P]
+    L.octax_step_host_frame.argtypes = [P, P, P, P, P, P, P]
     L.octax_gen_actions.argtypes = [P, u64, u64, P]
+    L.octax_rollout.argtypes = [P, ctypes.c_uint32, P, u64, u64, P, u64, P, P, P, P, u64]
     L.octax_stats.argtypes = [P, P]
     L.octax_stats_device.argtypes = [P, P]
     L.octax_get_state.argtypes = [P, u64, P]
@@ -221,6 +223,38 @@ class OctaxEnv:
         assert actions.dtype == np.int32 and actions.size == self.n
         _check(load_library().octax_step_host(self._h, p(actions), p(obs), p(reward), p(done),
                                               p(terminated), p(truncated)))
+
+    def rollout_into(self, T: int, obs, reward, done, actions=None, aseed: int = 0, t0: int = 0,
+                     terminated=None, truncated=None):
+        """Fused rollout (octax_rollout): T steps in one launch.  actions: int32 [T, n] or None
+        (in-kernel generator for steps t0..t0+T-1 under aseed).  obs: uint8 [T, n, 4, 32, 8]
+        (every step kept) or [n, 4, 32, 8] (overwritten; the last step remains); reward / done /
+        terminated / truncated: [T, n] or [n], likewise."""
+        import torch
+        n, T = self.n, int(T)
+        ob = 1024 * n
+        if obs.numel() not in (ob, T * ob):
+            raise ValueError(f"obs must hold n or T*n packed observations, got {obs.numel()} bytes")
+        obs_stride = ob if obs.numel() == T * ob and T > 1 else 0
+        outs = [reward, done, terminated, truncated]
+        sizes = {t.numel() for t in outs if t is not None}
+        if len(sizes) != 1 or sizes.pop() not in (n, T * n):
+            raise ValueError("reward / done / terminated / truncated must all be [n] or all [T, n]")
+        out_stride = n if reward.numel() == T * n and T > 1 else 0
+        _check(load_library().octax_rollout(
+            self._h, T, _dptr(actions, torch.int32, T * n), aseed & (2**64 - 1), t0,
+            _dptr(obs, torch.uint8), obs_stride, _dptr(reward, torch.float32), _dptr(done, torch.uint8),
+            _dptr(terminated, torch.uint8), _dptr(truncated, torch.uint8), out_stride))
+
+    def step_host_frame(self, actions: np.ndarray, frame: np.ndarray, reward: np.ndarray, done: np.ndarray,
+                        terminated: np.ndarray | None = None, truncated: np.ndarray | None = None):
+        """Host-buffer step shipping only the newest display (octax_step_host_frame): frame is
+        uint8 [n, 32, 8]; the stacked obs is [d(t-3), d(t-2), d(t-1), frame], all four = frame
+        where done (see include/octax.h)."""
+        p = lambda a: None if a is None else ctypes.c_void_p(a.ctypes.data)
+        assert actions.dtype == np.int32 and actions.size == self.n and frame.size == 256 * self.n
+        _check(load_library().octax_step_host_frame(self._h, p(actions), p(frame), p(reward), p(done),
+                                                    p(terminated), p(truncated)))
 
     def gen_actions(self, aseed: int, t: int, out):
         import torch

@@ -9,7 +9,7 @@ GAMES=${GAMES:-"pong_standin brix_standin target_shooter_level1"}
 for r in $(seq $ROUNDS); do
   for so in ab/*.so; do
     for g in $GAMES; do
-      v=$(OCTAX_LIB=$PWD/$so timeout 300 python bench.py --no-e2e --no-cpu --no-sweep --game $g --steps 20 --warmup 5 $EXTRA 2>/dev/null \
+      v=$(OCTAX_LIB=$PWD/$so timeout 300 python bench.py --no-e2e --no-cpu --no-sweep --no-fused --game $g --steps 20 --warmup 5 $EXTRA 2>/dev/null \
           | python -c "import json,sys; print('%.4g' % json.loads(sys.stdin.read())['value'])")
       echo "round $r $(basename $so) $g $v"
     done

@@ -50,7 +50,11 @@ MIXED = [("4", g, 262144, 0, "random") for g in ("pong_standin", "brix_standin",
         [("5", g, 1048576, 0, "random") for g in ("pong_standin", "target_shooter_level3")]
 
 
-def rollouts(game, n, obs_format, mode, reps, T=100, warm=0):
+def rollouts(game, n, obs_format, mode, reps, T=100, warm=0, launch="step"):
+    """Median / IQR steps/s of `reps` timed 100-step rollouts after one untimed one.  launch:
+    "step" = 100 octax_step launches; "graph" = the same 100 launches captured in one CUDA graph;
+    "fused" = one octax_rollout launch (in-kernel actions for random mode; a constant-action
+    rollout passes the zero [T][n] action buffer)."""
     rom, spec = workloads.game(game, obs_format=obs_format)
     s = torch.cuda.Stream()
     env = OctaxEnv(rom, spec, n, workloads.ENV_SEED, stream=s)
@@ -71,19 +75,79 @@ def rollouts(game, n, obs_format, mode, reps, T=100, warm=0):
                 env.gen_actions(workloads.ACTION_SEED, 0, acts[0])
             else:
                 acts[0].zero_()
+    g = None
+    if launch == "graph":
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for t in range(T):
+                env.step_into(acts[t], obs, rew, done)
     times = []
     for r in range(reps + 1):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
-        for t in range(T):
-            env.step_into(acts[t], obs, rew, done)
+        if launch == "graph":
+            with torch.cuda.stream(s):
+                g.replay()
+        elif launch == "fused":
+            with torch.cuda.stream(s):
+                env.rollout_into(T, obs, rew, done, actions=None if mode == "random" else acts,
+                                 aseed=workloads.ACTION_SEED, t0=0)
+        else:
+            for t in range(T):
+                env.step_into(acts[t], obs, rew, done)
         e1.record(s)
         e1.synchronize()
         if r > 0:  # first rollout is the warm-up
             times.append(e0.elapsed_time(e1) / 1e3)
+    del g
     env.close()
     sps = np.array([n * T / t for t in times])
     return float(np.median(sps)), float(np.percentile(sps, 75) - np.percentile(sps, 25))
+
+
+# SURVEY d.8 "bitexact, n_envs_checked, steps_checked": the GPU parity test that covers each
+# configuration with the same kernels and input recipe (its pass/fail is read from the pytest log
+# of the same box run, gpurun_out/pytest_gpu.log, when present)
+BITEXACT = {
+    "1": ("tests/test_gpu_parity.py::test_coverage_rom_n1_1000_steps_full_state_every_step", 1, 1000),
+    "2": ("tests/test_gpu_rollout.py::test_rollout_equals_steps_on_gpu_at_4096 + test_game_parity[pong_standin-300]", 300, 300),
+    "2*": ("tests/test_gpu_parity.py::test_game_parity[pong_standin-300]", 300, 300),
+    "3": ("tests/test_gpu_parity.py::test_game_parity[brix_standin-257] + test_bool_obs_startup_and_truncation_parity", 257, 300),
+    "4": ("tests/test_gpu_parity.py::test_config4_sampled_parity_1000_steps (64 sampled envs per game)", 64, 1000),
+    "5": ("tests/test_gpu_parity.py::test_full_size_sampled_parity (64 sampled envs at 1M) + "
+          "tests/test_gpu_rollout.py::test_rollout_1M_sampled_parity_and_step_equivalence", 64, 100),
+}
+
+
+def pytest_status():
+    try:
+        tail = open(os.path.join(ROOT, "gpurun_out", "pytest_gpu.log")).read().strip().splitlines()[-3:]
+    except OSError:
+        return "not run on this box"
+    t = " ".join(tail)
+    return "pass" if "failed" not in t and "passed" in t else "FAIL: " + t[-200:]
+
+
+def ncu_model(game, n):
+    """I_step, ALU-pipe instructions, eta and DRAM bytes per env step from the committed ncu
+    capture of THIS build (device-code digest) for this game and env count, else None."""
+    import glob
+    from paper_2510_01764_b200 import octax
+    from paper_2510_01764_b200.build import device_code_digest
+    have = device_code_digest(octax.SO_PATH)
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*step_full*.json"))):
+        try:
+            j = json.load(open(f))
+        except Exception:
+            continue
+        if j.get("sass_sha256") == have and j.get("game") == game and j.get("envs") == n:
+            return {"I_step_warp": j.get("warp_instr_per_env_step"),
+                    "I_step_thread": (j.get("warp_instr_per_env_step") or 0) * 32 * (j.get("warp_exec_efficiency") or 0),
+                    "alu_warp_instr_per_env_step": j.get("alu_warp_instr_per_env_step"),
+                    "eta": j.get("warp_exec_efficiency"), "dram_bytes_per_step": j.get("dram_bytes_per_env_step"),
+                    "source": os.path.relpath(f, ROOT)}
+    return None
 
 
 def main():
@@ -110,19 +174,52 @@ def main():
         hbm_gbs = 6650.0
     rows = []
     cpu_cache = {}
+    status = pytest_status()
+    cpu_model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu_model = next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
+    except Exception:
+        pass
+    from bench import ClockSampler
+    jobs = []
     for cid, game, n, fmt, mode, warm in [c + (0,) for c in CONFIGS] + [c + (1000,) for c in MIXED]:
-        med, iqr = rollouts(game, n, fmt, mode, args.reps, warm=warm)
+        launches = ["step", "fused"] if fmt == 0 else ["step"]  # octax_rollout: packed obs only
+        if n <= 65536 and not warm:
+            launches.append("graph")
+        jobs += [(cid, game, n, fmt, mode, warm, ln) for ln in launches]
+    for cid, game, n, fmt, mode, warm, launch in jobs:
+        with ClockSampler(0) as clk:
+            med, iqr = rollouts(game, n, fmt, mode, args.reps, warm=warm, launch=launch)
+        ck = clk.summary()
+        f_sm = (ck["sm_mhz"] or 1965.0) * 1e6
         rom, spec = workloads.game(game)
         cyc = spec["frame_skip"] * spec["instructions_per_frame"]
+        nm = ncu_model(game, n) if launch == "step" and fmt == 0 else None
+        # SURVEY d.2 roofs: issue = 148 SMs x 4 schedulers x 1 warp instr / cycle; ALU pipe = 148 x 4 x
+        # 1 warp instr / 2 cycles; each / the measured warp instructions per env step
+        R_issue = 148 * 4 * f_sm / nm["I_step_warp"] if nm and nm["I_step_warp"] else None
+        R_alu = 148 * 4 * 0.5 * f_sm / nm["alu_warp_instr_per_env_step"] if nm and nm["alu_warp_instr_per_env_step"] else None
+        R_hbm = hbm_gbs * 1e9 / 2201 if not fmt else None  # 2,201 algorithmic B / env step
+        roofs = {k: v for k, v in (("issue", R_issue), ("alu", R_alu), ("hbm", R_hbm)) if v}
+        binding = min(roofs, key=roofs.get) if roofs else None
+        bt, be, bs = BITEXACT.get(cid, ("", 0, 0))
         row = {"config": cid, "game": game, "rom": rom_label(game, rom), "envs": n, "gpus": 1,
-               "obs": "bool" if fmt else "packed", "mode": "step", "actions": mode,
+               "obs": "bool" if fmt else "packed", "mode": launch, "actions": mode,
                "protocol": "mixed" if warm else "fresh", "warmup_steps": warm + 100,
                "steps_per_rollout": 100, "reps": args.reps,
                "steps_per_s_median": med, "steps_per_s_iqr": iqr, "frames_per_s_median": 4 * med,
                "emu_instr_per_s": cyc * med,
-               # HBM roof of the packed path (2,201 algorithmic bytes per env step)
-               "R_hbm": hbm_gbs * 1e9 / 2201 if not fmt else None,
-               "bitexact": "pass: tests/test_gpu_parity.py (same kernels, same recipe)"}
+               "sm_clock_mhz_during": ck["sm_mhz"], "clock_reasons": ck["reasons"],
+               "dram_bytes_per_step_ncu": nm and nm["dram_bytes_per_step"], "I_step_ncu": nm and nm["I_step_thread"],
+               "I_step_warp_ncu": nm and nm["I_step_warp"], "eta_ncu": nm and nm["eta"],
+               "ncu_source": nm["source"] if nm else "no ncu capture of this build at this game / env count",
+               "R_issue": R_issue, "R_alu": R_alu, "R_hbm": R_hbm, "binding": binding,
+               "frac_binding": med / roofs[binding] if binding else None,
+               "bitexact": status, "bitexact_test": bt, "n_envs_checked": be, "steps_checked": bs,
+               "cpu_model": cpu_model}
+        # self-consistency: steps/s recomputes from the row's own fields
+        assert abs(row["frames_per_s_median"] - 4 * row["steps_per_s_median"]) < 1e-6 * row["frames_per_s_median"]
         if not args.no_cpu and game not in cpu_cache:
             one, _ = oracle_ref(game, 1)
             allc, C = oracle_ref(game, None)
@@ -135,15 +232,23 @@ def main():
     with open(args.out + ".json", "w") as f:
         json.dump({"device": dev, "protocol": "P:228, 1 warm-up + %d x 100-step rollouts" % args.reps,
                    "rows": rows}, f, indent=1)
-    lines = ["| config | game | envs | obs | actions | protocol | steps/s median | IQR | frames/s | oracle 1 core | oracle all cores (C) |",
-             "|---|---|---|---|---|---|---|---|---|---|---|"]
+    lines = ["| config | game | envs | obs | mode | actions | protocol | steps/s median | IQR | frames/s | SM MHz | "
+             "binding roof (frac) | bitexact (envs x steps) | oracle 1 core | oracle all cores (C) |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
-        lines.append(f"| {r['config']} | {r['game']} | {r['envs']:,} | {r['obs']} | {r['actions']} | {r['protocol']} | "
-                     f"{r['steps_per_s_median']:.4g} | {r['steps_per_s_iqr']:.3g} | {r['frames_per_s_median']:.4g} | "
+        roof = f"{r['binding']} ({r['frac_binding']:.2f})" if r["binding"] else "-"
+        lines.append(f"| {r['config']} | {r['game']} | {r['envs']:,} | {r['obs']} | {r['mode']} | {r['actions']} | "
+                     f"{r['protocol']} | {r['steps_per_s_median']:.4g} | {r['steps_per_s_iqr']:.3g} | "
+                     f"{r['frames_per_s_median']:.4g} | {r['sm_clock_mhz_during']} | {roof} | "
+                     f"{r['bitexact']} ({r['n_envs_checked']} x {r['steps_checked']}) | "
                      f"{r.get('oracle_1core', float('nan')):.3g} | {r.get('oracle_all_cores', float('nan')):.3g} ({r.get('cores', '-')}) |")
     with open(args.out + ".md", "w") as f:
-        f.write(f"# Paper protocol (P:228) on {dev}\n\n1 warm-up + {args.reps} timed 100-step rollouts per row; "
-                "CUDA events; device-resident actions.\n\n" + "\n".join(lines) + "\n")
+        f.write(f"# Paper protocol (P:228) on {dev}, host CPU {cpu_model}\n\n1 warm-up + {args.reps} timed 100-step "
+                "rollouts per row; CUDA events; device-resident actions (fused: generated in the kernel).  Modes "
+                "(SURVEY d.8): step = 100 octax_step launches, graph = the same launches in one CUDA graph, "
+                "fused = one octax_rollout launch.  Roofs (SURVEY d.2): issue / ALU pipe from the ncu capture of "
+                "this build at the row's game and env count, HBM from 2,201 algorithmic B per env step; "
+                "the full d.8 row is in the .json.\n\n" + "\n".join(lines) + "\n")
     print("\n".join(lines))
 
 

@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 N = 4096
 COMMON = ["--game", "brix_standin", "--steps", "20", "--warmup", "3", "--rollout", "8", "--max-episode-steps", "7",
-          "--no-sweep", "--no-e2e", "--no-cpu"]
+          "--no-sweep", "--no-e2e", "--no-cpu", "--no-fused"]
 
 
 def _port():

@@ -725,3 +725,34 @@ def test_stack_frames_startup_quirks_parity(obs_format, quirks):
                 startup=[(1 << 5, 2), (0, 3)], obs_format=obs_format, frame_skip=3)
     g, _ = _run_parity(rom, spec, 333, 60, 41 + quirks, 4, check_every=10)
     assert g.stats()[0][1] > 333
+
+
+@pytest.mark.parametrize("game,n,startup", [("brix_standin", 333, None), ("pong_standin", 130, [(1 << 1, 3)])])
+def test_step_host_frame_reconstructs_obs(game, n, startup):
+    """octax_step_host_frame ships only the newest display; a host history started from the reset
+    obs and rebuilt as [d(t-3), d(t-2), d(t-1), frame] (all four = frame where done, A10) equals
+    the oracle's stacked obs at every step, and reward / done / terminated / truncated match."""
+    over = dict(max_episode_steps=9)
+    if startup:
+        over["startup"] = startup
+    rom, spec = workloads.game(game, **over)
+    g = _gpu_env(rom, spec, n, 17)
+    o = oracle.OracleEnv(rom, spec, n, 17)
+    hist = g.reset(17).cpu().numpy().reshape(n, 4, 256)[:, 1:].copy()  # d(t-3), d(t-2), d(t-1)
+    o.reset(17)
+    na = workloads.n_actions(spec)
+    frame = np.zeros((n, 32, 8), np.uint8)
+    rew, done = np.zeros(n, np.float32), np.zeros(n, np.uint8)
+    term, trunc = np.zeros(n, np.uint8), np.zeros(n, np.uint8)
+    for t in range(40):
+        acts = np.ascontiguousarray(workloads.gen.actions(23, t, n, na))
+        g.step_host_frame(acts, frame, rew, done, term, trunc)
+        f = frame.reshape(n, 256)
+        obs = np.concatenate([hist, f[:, None]], axis=1)
+        obs[done != 0] = f[done != 0][:, None]
+        oo, orw, od, ot, otr = o.step(acts)
+        assert np.array_equal(obs.reshape(n, -1), oo), t
+        assert np.array_equal(rew, orw) and np.array_equal(done, od), t
+        assert np.array_equal(term, ot) and np.array_equal(trunc, otr), t
+        hist = obs[:, 1:].copy()
+    assert o.stats()[0][1] > 0  # truncations / resets happened
