@@ -20,6 +20,9 @@
  *   5. auto-reset finished envs in the same step, running the startup segments
  *      (P:146, P:158 startup_instructions; A10 Gymnax convention: the returned
  *      obs is the reset obs; reward/done come from the terminal transition).
+ *      This deviates from SPEC S:409's "final observation, then reset before the
+ *      next step": the terminal obs SPEC would return is available as
+ *      octax_step_ex's final_obs_out (written for done envs).
  * Readings A1..A27 are listed in DESIGN.md.
  *
  * Memory: the library owns all VM state (device memory of the handle's device).

@@ -34,8 +34,12 @@ def opcode(sass: str) -> str:
     return s.split(None, 1)[0].split(".")[0] if s else ""
 
 
+EMBEDDED = {}  # file -> {line: text}, the source the capture was taken from (--import-source on)
+
+
 def markers(path):
-    """(line, title) markers of a source file."""
+    """(line, title) markers of a source file: from the source embedded in the report when it has
+    one (so regions match the profiled build even after the file changed), else the file on disk."""
     out = []
     try:
         lines = open(path).read().splitlines()
@@ -62,7 +66,47 @@ def markers(path):
     return sorted(set(out))
 
 
+REMAP = {}  # file -> {line in the profiled build: line in the file on disk}
+
+
+def remap_lines(path):
+    """Map the profiled build's line numbers (source embedded in the report: only lines that carry
+    code) onto the file on disk by matching line texts near a running offset, so the region
+    markers (comments, which the report does not embed) still apply after the file changed."""
+    emb = EMBEDDED.get(path)
+    try:
+        cur = open(path).read().splitlines()
+    except OSError:
+        return {}
+    if not emb:
+        return {}
+    m, off = {}, 0
+    for ln in sorted(emb):
+        t = emb[ln].strip()
+        j = ln + off - 1
+        if 0 <= j < len(cur) and cur[j].strip() == t:
+            m[ln] = j + 1
+            continue
+        best = None
+        for d in range(1, 200):
+            for k in (j - d, j + d):
+                if 0 <= k < len(cur) and t and cur[k].strip() == t:
+                    best = k
+                    break
+            if best is not None:
+                break
+        if best is not None:
+            off = best - (ln - 1)
+            m[ln] = best + 1
+        else:
+            m[ln] = ln + off
+    return m
+
+
 def region_of(file, line, cache):
+    if file not in REMAP:
+        REMAP[file] = remap_lines(file)
+    line = REMAP[file].get(line, line)
     if file not in cache:
         cache[file] = markers(file)
     best = None
@@ -95,6 +139,12 @@ def main():
                 except (ValueError, IndexError):
                     pass
                 break
+    efile = None
+    for row in csv.reader(io.StringIO(txt)):
+        if row and row[0] == "File Path":
+            efile = row[1]
+        elif row and row[0].isdigit() and len(row) > 1 and efile:
+            EMBEDDED.setdefault(efile, {})[int(row[0])] = row[1]
     seen = set()  # an address listed under two source lines (inlining) counts once
     agg = collections.defaultdict(lambda: collections.Counter())
     ops = collections.defaultdict(collections.Counter)

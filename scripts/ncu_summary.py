@@ -29,6 +29,9 @@ KEY_METRICS = [
     "dram__bytes_read.sum",
     "dram__bytes_write.sum",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__t_requests_pipe_lsu_mem_local_op_ld.sum",
+    "l1tex__t_requests_pipe_lsu_mem_local_op_st.sum",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum",
     "l1tex__t_bytes_pipe_lsu_mem_local_op_ld.sum",
