@@ -487,17 +487,8 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   const bool ex = RF ? act : true;  // gate of the flag-driven effects
   // warp votes for the gated classes, taken as soon as the entry is known so the branches at
   // the end of the core do not wait on them (A/B +1%)
-#ifdef OCTAX_REDUX_VOTE
-  // one warp OR of the executing lanes' flags answers every vote-gated class test uniformly
-  const uint32_t wflags = __reduce_or_sync(kFull, ex ? d : 0u);
-  const bool any_rare = (wflags & D_RARE) != 0u;
-  const bool any_draw = (wflags & D_DRAW) != 0u;
-#define ANY_CLASS(pred, F) ((wflags & (F)) != 0u)
-#else
   const bool any_rare = __any_sync(kFull, ex && HAS(d, D_RARE));
   const bool any_draw = __any_sync(kFull, ex && HAS(d, D_DRAW));
-#define ANY_CLASS(pred, F) __any_sync(kFull, pred)
-#endif
   // V[k] of this lane lives at vbase | voff(k) (VREG); kx = V[x], or V0 for BNNN
   const uint32_t vb = vbase(tid), ax = (e.y & 0x1FFu) | vb, vx = sm.V[ax], vy = sm.V[((e.y >> 9) & 0x1FFu) | vb];
   OCTAX_CHECK(ax < 16u * kBlock && (((e.y >> 9) & 0x1FFu) | vb) < 16u * kBlock);
@@ -561,20 +552,20 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   const bool do_cls = ex && HAS(d, E_CLS);
   const bool do_rnd = ex && HAS(d, D_RND);
   const bool do_mem = ex && HAS(d, D_MEM);
-  if (ANY_CLASS(do_cls, E_CLS)) {
+  if (__any_sync(kFull, do_cls)) {
     if (do_cls) {
 #pragma unroll
       for (int r = 0; r < 32; ++r) sm.fb[tid * 32 + r] = 0;
     }
   }
-  if (ANY_CLASS(do_rnd, D_RND)) {
+  if (__any_sync(kFull, do_rnd)) {
     if (do_rnd) {
       const uint32_t r = philox_out0(L.draw, L.episode, gid, 0u, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
       VREG(x) = (uint8_t)(r & nn);
       L.draw++;
     }
   }
-  if (ANY_CLASS(do_mem, D_MEM)) {
+  if (__any_sync(kFull, do_mem)) {
     if (do_mem) {
       if (f33) {
         wr(sm, p, L, L.I & 0xFFFu, vx / 100u);
@@ -811,10 +802,6 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       for (uint32_t k = 0; k < p.ipf; ++k) {
         const bool cp = cur < ne;
         uint4 q;  // only read under cp
-#ifdef OCTAX_COPY_IDX
-        rp = rsrc + cur * 16;  // one IMAD.WIDE each instead of two 64-bit pointer increments
-        opl = odst + cur * 128;
-#endif
         if (cp) q = __ldcs(rp);
         // L1 prefetch of the chunk two cycles ahead (from the L2-resident ring block): its load
         // is then an L1 hit, and the store at the end of that cycle does not wait on L2 (A/B:
@@ -841,10 +828,6 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     }
     // envs the per-cycle copy did not reach (fewer than 32 cycles per step): rp / opl already point
     // at env `cur`, so the ring / obs bases need not stay live through the frame loop
-#ifdef OCTAX_COPY_IDX
-    rp = rsrc + cur * 16;
-    opl = odst + cur * 128;
-#endif
 #pragma unroll 4
     for (int e = cur; e < ne; ++e, rp += 16, opl += 128) put_rows(opl, 0u, l2 ^ ((uint32_t)e & kSwz), __ldcs(rp));
     if (active) L.halted = !L.run;
