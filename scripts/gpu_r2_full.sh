@@ -21,10 +21,19 @@ for ENVS in 1048576 262144; do
   python scripts/ncu_summary.py full gpurun_out/$TAG.ncu-rep gpurun_out/step_$TAG.json --envs $ENVS --game pong_standin --so $SO > /dev/null 2>&1
 done
 cp gpurun_out/step_full_1048576.json profiles/latest_step_full.json && echo "latest_step_full refreshed"
+# the other games at configs[3]'s 262,144 envs (per-game instruction counts for the protocol rows)
+for G in ${NCU_GAMES:-brix_standin target_shooter_level1 target_shooter_level2 target_shooter_level3}; do
+  TAG=full_${G}_262144
+  PCMD="python bench.py --steps 3 --warmup 3 --envs 262144 --game $G --no-sweep --no-e2e --no-cpu --no-fused"
+  timeout 300 $PCMD > gpurun_out/plain_$TAG.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:octax_kernel -s 5 -c 1 -o gpurun_out/$TAG -f $PCMD > gpurun_out/ncu_$TAG.log 2>&1
+  echo "ncu $TAG rc=$?"
+  python scripts/ncu_summary.py full gpurun_out/$TAG.ncu-rep gpurun_out/step_$TAG.json --envs 262144 --game $G --so $SO > /dev/null 2>&1
+done
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 if [ -n "$LAUNCHES" ]; then
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-    python bench.py --no-sweep > gpurun_out/ncu_launch.log 2>&1; echo "launch list rc=$?"
+    python bench.py --no-sweep --no-fused > gpurun_out/ncu_launch.log 2>&1; echo "launch list rc=$?"
 fi
 if [ -n "$PROTOCOL" ]; then
   timeout 2400 python scripts/paper_protocol.py --out gpurun_out/paper_protocol > gpurun_out/protocol.log 2>&1; echo "protocol rc=$?"
