@@ -70,7 +70,7 @@ struct __align__(128) Smem {
   uint64_t fb[kBlock * 32];                  // framebuffer rows, bit 63-x = pixel x, swizzled
   uint8_t V[16 * kBlock];                    // V[k] of env t: its own bank (see vbase / VREG)
   uint16_t stk[16 * kBlock];                 // stk[k*kBlock + tid]
-  uint32_t dprm[kBlock / 32][33];            // DXYN owner params (x0 | y0 << 6 | base << 11); [32] = unread
+  uint32_t dprm[kBlock / 32][32];            // DXYN owner params (x0 | y0 << 6 | base << 11)
   uint8_t down[kBlock / 32][32];             // DXYN item -> owner lane map
   unsigned long long red[4][kBlock / 32];    // per-warp statistics
   unsigned long long bar;                    // mbarrier for the image copy
@@ -219,18 +219,6 @@ __device__ __forceinline__ void set_keys(Lane &L, uint32_t km) {
 // compiler from lowering a single-bit test to shift + and + compare (one LOP3 instead).
 constexpr uint32_t kPad = 1u << 24;
 #define HAS(d, F) (((d) & ((F) | kPad)) != 0u)
-
-// dst = (flags & mask) != 0 ? src : dst.  OCTAX_PMOV: written as a flag test and a PREDICATED MOVE
-// so ptxas can issue the move on the FMA pipe (IMAD.MOV) instead of a SEL on the ALU pipe, the
-// binding one (both pipes take one warp instruction per 2 cycles per SMSP; FMA runs at ~14%)
-__device__ __forceinline__ void pmov(uint32_t &dst, uint32_t flags, uint32_t mask, uint32_t src) {
-#ifdef OCTAX_PMOV
-  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.b32 p, t, 0;\n\t@p mov.b32 %0, %3;\n\t}"
-      : "+r"(dst) : "r"(flags), "r"(mask), "r"(src));
-#else
-  dst = (flags & (mask | kPad)) != 0u ? src : dst;
-#endif
-}
 
 
 __device__ __forceinline__ uint32_t rd(const Smem &sm, const StepParams &p, const Lane &L, uint32_t a) {
@@ -442,55 +430,6 @@ __device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepP
   if (vfw) VREG(15) = (uint8_t)(mine && ((hb >> (rank * m)) & ((1u << m) - 1u)) != 0u);
 }
 
-// DXYN in fixed groups of 8 lanes, several passes (OCTAX_DRAW8 A/B): the k drawers publish their
-// parameters by rank; pass j0 / 4 serves drawers j0..j0+3, lane r of group g XORing row r (< 8) of
-// drawer j0 + g.  VF of the drawer comes from its group's 8 bits of the pass's ballot.
-template <bool DIRTY, bool SCAT>
-__device__ __forceinline__ void draw_groups8(Smem &sm, const Lane &L, const StepParams &p, int tid, int lane,
-                                             uint64_t block0, uint32_t dm, uint32_t x0, uint32_t y0, uint32_t base,
-                                             uint32_t nrows, bool wdirty, uint32_t quirks, bool vfw) {
-  const bool wrap = (quirks & 8u) != 0;
-  const uint32_t warp = (uint32_t)tid >> 5, wl = (uint32_t)tid & ~31u;
-  const bool mine = ((dm >> lane) & 1u) != 0u;
-  const uint32_t rank = (uint32_t)__popc(dm & ((1u << lane) - 1u));
-  sm.dprm[warp][mine ? rank : 32u] = x0 | (y0 << 6) | (base << 11) | (nrows << 23) | ((uint32_t)lane << 27);
-  __syncwarp();
-  const uint32_t k = (uint32_t)__popc(dm), g = (uint32_t)lane >> 3, r = (uint32_t)lane & 7u;
-  bool vf = false;
-  for (uint32_t j0 = 0; j0 < k; j0 += 4) {
-    const uint32_t j = j0 + g;
-    const uint32_t q = j < k ? sm.dprm[warp][j] : 0u;
-    const uint32_t own = q >> 27, oe = wl + own;
-    uint64_t od = 0;
-    const uint8_t *oram = nullptr;  // owner's RAM backing
-    if (DIRTY) {
-      od = __shfl_sync(kFull, L.dirty, own);
-      oram = SCAT ? reinterpret_cast<const uint8_t *>(__shfl_sync(kFull, reinterpret_cast<unsigned long long>(L.ram), own))
-                  : p.s.ram + (block0 + oe) * 4096ull;
-    }
-    bool hit = false;
-    if (r < ((q >> 23) & 15u)) {
-      const uint32_t ox = q & 63u, a = ((q >> 11) & 0xFFFu) + r;
-      uint32_t byte = 0;
-      if (DIRTY) {
-        if (a <= 0xFFFu) byte = ((od >> (a >> 6)) & 1ull) ? (uint32_t)oram[a] : IMG(a);
-      } else {
-        byte = a <= 0xFFFu ? IMG(a) : 0u;
-      }
-      const uint32_t yy = (((q >> 6) & 31u) + r) & 31u, q8 = ox & 0x38u;
-      const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> (ox & 7u), 0, 0x4401);
-      const uint64_t mk = wrap ? ((w << q8) | (q8 ? (w >> (64u - q8)) : 0ull)) : (w << q8);
-      uint64_t *row = &sm.fb[oe * 32u + (yy ^ (oe & kSwz))];
-      const uint64_t old = *row;
-      *row = old ^ mk;
-      hit = (old & mk) != 0ull;
-    }
-    const uint32_t hb = __ballot_sync(kFull, hit);
-    vf = (rank >> 2) == (j0 >> 2) ? ((hb >> (8u * (rank & 3u))) & 0xFFu) != 0u : vf;
-  }
-  if (vfw) VREG(15) = (uint8_t)(mine && vf);
-}
-
 // DXYN when no lane of the warp draws more than one row (a 1-row sprite, or clipped at
 // the bottom): one row step, no sprite-word realignment.
 template <bool DIRTY>
@@ -585,22 +524,22 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   // ---- register writes
 
   uint32_t nvx = nn;
-  pmov(nvx, d, D_VSADD, vx + nn);
-  pmov(nvx, d, D_VSALU, r8);
-  pmov(nvx, d, D_VSDT, L.dt);
-  pmov(nvx, d, D_WAIT, L.kidx);
+  nvx = HAS(d, D_VSADD) ? (vx + nn) : nvx;
+  nvx = HAS(d, D_VSALU) ? r8 : nvx;
+  nvx = HAS(d, D_VSDT) ? L.dt : nvx;
+  nvx = HAS(d, D_WAIT) ? L.kidx : nvx;
   sm.V[ax] = (uint8_t)((ex && (d & L.wvm) != 0u) ? nvx : vx);  // unconditional: no branch around the ALU
   if (ex && HAS(d, D_WVF)) VREG(15) = (uint8_t)f8;
   // ---- control flow and index / timer registers
   uint32_t npc = pc + 2u + skip2;
-  pmov(npc, d, D_PCJ, nnn);  // 1NNN, 2NNN
+  npc = HAS(d, D_PCJ) ? nnn : npc;  // 1NNN, 2NNN
   npc = is_ret ? ret_pc : npc;
-  pmov(npc, d, L.stay, pc);  // A16: FX0A re-executes while no key; E_BAD stays
-  pmov(npc, d, D_BJMP, (nnn + vx) & 0xFFFu);  // vx = V0 or V[x] (JUMP_VX quirk)
+  npc = (d & L.stay) != 0u ? pc : npc;  // A16: FX0A re-executes while no key; E_BAD stays
+  npc = HAS(d, D_BJMP) ? ((nnn + vx) & 0xFFFu) : npc;  // vx = V0 or V[x] (JUMP_VX quirk)
   uint32_t I2 = L.I;
-  pmov(I2, d, D_INNN, nnn);
-  pmov(I2, d, D_IADD, I2 + vx);  // 16-bit I kept modulo 2^32: users mask (A18)
-  pmov(I2, d, D_IFONT, 0x50u + 5u * (vx & 15u));
+  I2 = HAS(d, D_INNN) ? nnn : I2;
+  I2 = HAS(d, D_IADD) ? (I2 + vx) : I2;  // 16-bit I kept modulo 2^32: users mask (A18)
+  I2 = HAS(d, D_IFONT) ? (0x50u + 5u * (vx & 15u)) : I2;
   L.pc = act ? npc : pc;  // PC <= 0xFFE when running; halted-at-entry lanes carry bit 16 (see kDecEntries)
   L.dec = __ldg(p.s.dec + L.pc);  // next cycle's word, in flight meanwhile (re-read when idle)
   L.I = ex ? I2 : L.I;
@@ -652,17 +591,6 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     const uint32_t dm = __ballot_sync(kFull, nrows != 0u);
     // one grouped pass (groups of maxr lanes, 32 / maxr drawers) when the drawers fit and
     // rows are many enough to beat maxr lane-parallel row steps (uniform choice)
-#ifdef OCTAX_DRAW8
-    // sprites of 2..8 rows: fixed groups of 8 lanes, ceil(k / 4) passes, unless maxr lane-parallel
-    // row steps are cheaper (few rows, many drawers) -- a uniform cost comparison
-    const uint32_t kd = (uint32_t)__popc(dm);
-    if (maxr >= 2u && maxr <= 8u && 2u * ((kd + 3u) >> 2) <= maxr) {
-      if (wdirty)
-        draw_groups8<true, SCAT>(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, wdirty, quirks, do_draw);
-      else
-        draw_groups8<false, SCAT>(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, wdirty, quirks, do_draw);
-    } else
-#endif
     if (maxr >= 3u && (uint32_t)__popc(dm) * maxr <= 32u)  // k drawers fit 32 / maxr groups
     {
       if (wdirty)
