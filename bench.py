@@ -543,8 +543,19 @@ def main():
         fenv.close()
         tf = float(odist.max_over_ranks(torch.tensor([tm], dtype=torch.float64, device="cuda")).item())
         fv = world * n * 100 * R / (tf / 1e3)
+        # its rooflines: HBM with the fused mode's 1,797 algorithmic B per env step (no state round
+        # trip, no framebuffer TMA read, in-kernel actions), ALU pipe with the step
+        # kernel's measured instruction count (the same interpreter; an upper bound)
+        f_bytes = 512 + 1024 + 256 + 4 + 1
+        hbm_f = f_bytes * fv / world / 1e9
+        fused_roof = {"hbm": {"achieved": hbm_f, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_f / hbm_peak,
+                              "alg_bytes_per_env_step": f_bytes}}
+        if alu:
+            a_f = alu["alu_warp_instr_per_env_step"] * 32 * fv / world / 1e9
+            fused_roof["alu"] = {"achieved": a_f, "peak": alu["peak"], "frac": a_f / alu["peak"],
+                                 "note": "step kernel's ALU-pipe instructions per env step (upper bound)"}
         fused = {"mode": "fused", "steps_per_rollout": 100, "rollouts_timed": R, "warmup_rollouts": 1,
-                 "steps_per_s": fv, "frames_per_s": 4 * fv, "ms_per_step": tf / (100 * R),
+                 "steps_per_s": fv, "frames_per_s": 4 * fv, "ms_per_step": tf / (100 * R), "roofline": fused_roof,
                  "ms_per_rollout_median": sorted(per_r)[len(per_r) // 2],
                  "vs_step_mode": fv / value, "stats": [int(x) for x in fst.cpu().tolist()],
                  "actions": "generated inside the rollout kernel (Philox domain 1, same stream as octax_gen_actions)",
