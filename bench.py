@@ -604,8 +604,15 @@ def main():
                                    workloads.ACTION_SEED, torch, OctaxEnv, barrier)
             tt = float(odist.max_over_ranks(torch.tensor([tm], dtype=torch.float64, device="cuda")).item())
             sps = world * m * args.steps / (tt / 1e3)
-            games.append({"game": g, "envs_per_gpu": m, "steps_per_s": sps, "frames_per_s": 4 * sps,
-                          "source": "paper listing (App. D)" if g.startswith("target") else "labelled stand-in"})
+            row = {"game": g, "envs_per_gpu": m, "steps_per_s": sps, "frames_per_s": 4 * sps,
+                   "source": "paper listing (App. D)" if g.startswith("target") else "labelled stand-in"}
+            if not args.no_fused:  # the same workload as 100-step fused rollouts
+                tm, _, fenv = time_rollout(grom, gspec, m, 100, 2, 1, odist.shard(rank, world, m)[0],
+                                           workloads.ACTION_SEED, torch, OctaxEnv, barrier)
+                fenv.close()
+                tt = float(odist.max_over_ranks(torch.tensor([tm], dtype=torch.float64, device="cuda")).item())
+                row["steps_per_s_fused"] = world * m * 200 / (tt / 1e3)
+            games.append(row)
 
     # the oracle on the host cores, rank 0 only, after every rank's GPU work (the other ranks
     # wait at the closing barrier)

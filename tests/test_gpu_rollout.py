@@ -197,3 +197,34 @@ def test_rollout_1M_sampled_parity_and_step_equivalence():
         b.step(act)
     assert g.state_digests()[1] == b.state_digests()[1]
     assert np.array_equal(g.stats()[0], b.stats()[0])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("game", ["brix_standin", "target_shooter_level3"])
+def test_rollout_config4_sampled_parity_1000_steps(game):
+    """SURVEY d.1 config 4 in the fused mode: n = 262,144, ten 100-step rollouts with
+    in-kernel actions; after every rollout the config-4 sample (envs {0, 1, n/2, n-1} + 60
+    Philox-domain-2 ids, one oracle instance each) is compared in full canonical state, and the
+    last step's obs / reward / done of the sample as well; brix's terminations reset envs inside
+    the rollouts."""
+    rom, spec = workloads.game(game)
+    n, R, T = 262144, 10, 100
+    na = workloads.n_actions(spec)
+    g = _env(rom, spec, n, workloads.ENV_SEED)
+    key = [workloads.ENV_SEED & 0xFFFFFFFF, workloads.ENV_SEED >> 32]
+    ids = [0, 1, n // 2, n - 1] + [oracle.philox4x32_10([k, 0, 0, 2], key)[0] % n for k in range(60)]
+    oracles = [oracle.OracleEnv(rom, spec, 1, workloads.ENV_SEED, gid) for gid in ids]
+    idx = torch.tensor(ids, device="cuda")
+    obs, rew, done, _, _ = _outs(T, n, per_step=False)
+    for r in range(R):
+        g.rollout_into(T, obs, rew, done, aseed=workloads.ACTION_SEED, t0=r * T)
+        go = obs.reshape(n, -1)[idx].cpu().numpy()
+        gr, gd = rew[idx].cpu().numpy(), done[idx].cpu().numpy()
+        st = g.get_states(ids)
+        for k, gid in enumerate(ids):
+            for t in range(r * T, (r + 1) * T):
+                oo, orw, od, _, _ = oracles[k].step(
+                    np.array([oracle.synthetic_action(workloads.ACTION_SEED, t, gid, na)], np.int32))
+            assert np.array_equal(st[k], oracles[k].get_state(0)), (r, gid)
+            assert np.array_equal(go[k], oo[0]) and gr[k] == orw[0] and gd[k] == od[0], (r, gid)
+    assert g.stats()[0][2] == n * R * T
