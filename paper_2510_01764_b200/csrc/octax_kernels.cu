@@ -215,6 +215,14 @@ __device__ __forceinline__ void set_keys(Lane &L, uint32_t km) {
   L.stay = (km ? 0u : D_WAIT) | E_BAD;  // E_BAD: a faulting entry keeps its PC (cycle<Q0, false>)
   L.kidx = (uint32_t)(__ffs(km) - 1);
 }
+// XOR a sprite-row mask into a framebuffer row, returning the row's old value (VF = old & mask).
+// (Two native 32-bit ATOMS.XOR instead measured -0.3..-0.6%; sm_100 has no native 64-bit one.)
+__device__ __forceinline__ uint64_t xor_row(uint64_t *row, uint64_t m) {
+  const uint64_t old = *row;
+  *row = old ^ m;
+  return old;
+}
+
 // Flag test written with a two-bit mask (kPad is never set in an entry): keeps the
 // compiler from lowering a single-bit test to shift + and + compare (one LOP3 instead).
 constexpr uint32_t kPad = 1u << 24;
@@ -360,8 +368,7 @@ __device__ __forceinline__ void draw_lanes(Smem &sm, Lane &L, const StepParams &
       byte = r < nrows ? byte : 0u;
       const uint64_t m = (uint64_t)__byte_perm(byte << sl, 0, 0x4401) << q8;
       uint64_t *row = rows + (((y0 + r) & 31u) ^ swz);
-      const uint64_t old = *row;
-      *row = old ^ m;
+      const uint64_t old = xor_row(row, m);
       hit |= old & m;
     }
   } else {
@@ -371,8 +378,7 @@ __device__ __forceinline__ void draw_lanes(Smem &sm, Lane &L, const StepParams &
       const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> sh, 0, 0x4401);
       const uint64_t m = wrap ? ((w << q8) | (q8 ? (w >> (64u - q8)) : 0ull)) : (w << q8);
       uint64_t *row = rows + (((y0 + r) & 31u) ^ swz);
-      const uint64_t old = *row;
-      *row = old ^ m;
+      const uint64_t old = xor_row(row, m);
       hit |= old & m;
     }
   }
@@ -422,8 +428,7 @@ __device__ __forceinline__ void draw_groups(Smem &sm, const Lane &L, const StepP
     const uint64_t mk = wrap ? ((w << q8) | (q8 ? (w >> (64u - q8)) : 0ull)) : (w << q8);
     OCTAX_CHECK(oe < (uint32_t)kBlock && yy < 32u);
     uint64_t *row = &sm.fb[oe * 32u + (yy ^ (oe & kSwz))];
-    const uint64_t old = *row;
-    *row = old ^ mk;
+    const uint64_t old = xor_row(row, mk);
     hit = (old & mk) != 0ull;
   }
   const uint32_t hb = __ballot_sync(kFull, hit);
@@ -444,8 +449,7 @@ __device__ __forceinline__ void draw_one(Smem &sm, const StepParams &p, const La
     const uint64_t w = (uint64_t)__byte_perm((byte << 8) >> (x0 & 7u), 0, 0x4401);
     const uint64_t mk = (quirks & 8u) ? ((w << q8) | (q8 ? (w >> (64u - q8)) : 0ull)) : (w << q8);
     uint64_t *row = &sm.fb[(uint32_t)tid * 32u + (y0 ^ ((uint32_t)tid & kSwz))];
-    const uint64_t old = *row;
-    *row = old ^ mk;
+    const uint64_t old = xor_row(row, mk);
     hit = (old & mk) != 0ull;
   }
   if (vfw) VREG(15) = (uint8_t)hit;

@@ -30,6 +30,13 @@ for G in ${NCU_GAMES:-brix_standin target_shooter_level1 target_shooter_level2 t
   echo "ncu $TAG rc=$?"
   python scripts/ncu_summary.py full gpurun_out/$TAG.ncu-rep gpurun_out/step_$TAG.json --envs 262144 --game $G --so $SO > /dev/null 2>&1
 done
+if [ -n "$FUSED_NCU" ]; then  # one 100-step fused rollout launch (octax_kernel<2,1>) at 1M envs
+  PCMD="python bench.py --steps 3 --warmup 3 --envs 1048576 --no-sweep --no-e2e --no-cpu"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:octax_kernel -s 8 -c 1 \
+    -o gpurun_out/fused_1048576 -f $PCMD > gpurun_out/ncu_fused.log 2>&1; echo "ncu fused rc=$?"
+  python scripts/ncu_summary.py full gpurun_out/fused_1048576.ncu-rep gpurun_out/fused_full_1048576.json \
+    --envs 104857600 --game pong_standin --so $SO > /dev/null 2>&1
+fi
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 if [ -n "$LAUNCHES" ]; then
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
