@@ -84,3 +84,12 @@ def test_null_arguments(lib):
     assert lib.octax_step(None, None, None, None, None, None, None) == -1
     assert lib.octax_stats(None, None) == -1
     lib.octax_destroy(None)
+
+
+def test_gymnax_key_to_seed():
+    """Gymnax front end: reset keys map to the uint64 seed (int, or [hi, lo] uint32 words)."""
+    from paper_2510_01764_b200.gymnax_env import seed_from_key
+    assert seed_from_key(7) == 7 and seed_from_key(-1) == 2**64 - 1
+    assert seed_from_key([0x12345678, 0x9ABCDEF0]) == 0x123456789ABCDEF0
+    with pytest.raises(ValueError):
+        seed_from_key([1, 2, 3])

@@ -756,3 +756,30 @@ def test_step_host_frame_reconstructs_obs(game, n, startup):
         assert np.array_equal(term, ot) and np.array_equal(trunc, otr), t
         hist = obs[:, 1:].copy()
     assert o.stats()[0][1] > 0  # truncations / resets happened
+
+
+def test_gymnax_env_matches_oracle():
+    """OctaxGymnaxEnv (Gymnax call shapes, NEXT-3): reset(key) seeds like octax_reset(seed),
+    step(key, state, action) returns the oracle's obs / reward / done (bool x-major obs),
+    terminal obs in info where done; a stale EnvState is refused."""
+    from paper_2510_01764_b200.gymnax_env import OctaxGymnaxEnv, seed_from_key
+    rom, spec = workloads.game("brix_standin", max_episode_steps=6)
+    n = 100
+    env = OctaxGymnaxEnv(rom, spec, n)
+    key = [0x12345678, 0x9ABCDEF0]
+    o = oracle.OracleEnv(rom, dict(spec, obs_format=1), n, seed_from_key(key))
+    obs, state = env.reset(key, env.default_params)
+    assert np.array_equal(obs.cpu().numpy().reshape(n, -1).astype(np.uint8), o.reset(seed_from_key(key)))
+    na = env.num_actions
+    for t in range(10):
+        a = workloads.gen.actions(5, t, n, na)
+        old = state
+        obs, state, rew, done, info = env.step(None, state, torch.from_numpy(a))
+        oo, orw, od, ot, otr = o.step(a)
+        assert np.array_equal(obs.cpu().numpy().reshape(n, -1).astype(np.uint8), oo), t
+        assert np.array_equal(rew.cpu().numpy(), orw) and np.array_equal(done.cpu().numpy().astype(np.uint8), od)
+        assert np.array_equal(info["truncated"].cpu().numpy().astype(np.uint8), otr)
+    assert state.time == 10
+    with pytest.raises(ValueError):
+        env.step(None, old, torch.from_numpy(a))
+    env.close()
