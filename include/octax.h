@@ -203,6 +203,8 @@ octax_status octax_gen_actions(octax_env *e, uint64_t aseed, uint64_t t, int32_t
  *    every step overwrites the same [n] obs buffer, so the last step's obs remains), its
  *    reward / done / terminated / truncated to [t*out_step_stride + j] (elements; 0 = same
  *    buffers every step).  terminated_out / truncated_out may be NULL.  All DEVICE buffers.
+ *  - obs_out may be NULL: no observation is written (rewards / dones only, e.g. policy-free
+ *    evaluation); the display history is still kept, so later steps' obs are unaffected.
  *  - a non-zero stride must cover all n envs (obs: >= n * 1024 bytes; outputs: >= n).
  * Same-step auto-reset (A10) runs inline, also for specs with startup segments.  Packed obs
  * only: a handle created with OCTAX_OBS_BOOL_XMAJOR gets OCTAX_E_INVALID_ARG (either stacking

@@ -599,13 +599,14 @@ extern "C" octax_status octax_step_host(octax_env *e, const int32_t *actions_hos
 extern "C" octax_status octax_rollout(octax_env *e, uint32_t T, const int32_t *actions, uint64_t aseed, uint64_t t0,
                                       void *obs_out, uint64_t obs_step_stride, float *reward_out, uint8_t *done_out,
                                       uint8_t *terminated_out, uint8_t *truncated_out, uint64_t out_step_stride) {
-  if (!e || !obs_out || !reward_out || !done_out)
+  if (!e || !reward_out || !done_out)
     return set_err(OCTAX_E_INVALID_ARG, "NULL argument to octax_rollout");
   if (T == 0) return OCTAX_OK;
   if (e->obs_format != OCTAX_OBS_PACKED)
     return set_err(OCTAX_E_INVALID_ARG, "octax_rollout: packed observations only (obs_format OCTAX_OBS_PACKED)");
   if (obs_step_stride % 16 != 0)
     return set_err(OCTAX_E_INVALID_ARG, "octax_rollout: obs_step_stride must be a multiple of 16 bytes");
+  if (!obs_out) obs_step_stride = 0;
   if ((obs_step_stride != 0 && obs_step_stride < (uint64_t)e->obs_bytes * e->n) ||
       (out_step_stride != 0 && out_step_stride < e->n))
     return set_err(OCTAX_E_INVALID_ARG, "octax_rollout: a non-zero step stride must cover all n envs");

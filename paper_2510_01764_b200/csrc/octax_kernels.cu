@@ -749,6 +749,9 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   // throughout; each step's display goes to the ring with plain per-warp stores, so after the
   // prologue a warp needs no CTA barrier until the statistics at the end.
   const uint32_t T = MODE == MODE_ROLLOUT ? p.T : 1u;
+  // observations written?  Always in a step; a rollout may run without them (obs_out == NULL:
+  // rewards / dones only -- the ring history is still kept for the steps after it)
+  const bool wobs = MODE != MODE_ROLLOUT || obs != nullptr;
   for (uint32_t t = 0; t < T; ++t) {
   const uint32_t h = (p.head + t) & 3u;
   const uint32_t s0 = (h + 2) & 3, s1 = (h + 3) & 3, s2 = h;
@@ -771,7 +774,8 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     // this step; planes for frames before the step (frame_skip < 4) = step-start display.
     const bool sf = p.stack_frames != 0u;
     const int first = sf ? 4 - (int)p.frame_skip : 3;  // planes [0, first) <- step-start display
-    if (!sf) {
+    if (!wobs) {
+    } else if (!sf) {
       for (int e = 0; e < ne; e += 2)  // plane 2 <- step-start display, two envs per pass
         if (e + (int)hh < ne) {
           const uint32_t el = (uint32_t)(warp * 32 + e) + hh;
@@ -794,11 +798,11 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     const uint4 *rsrc = reinterpret_cast<const uint4 *>(ring_at(p, hh ? s1 : s0, wbase) + l2);
     // one bulk L2 prefetch per half-warp of its 8 KB ring block (plane 0 or 1 of the warp's
     // 32 envs): the per-cycle copy loads then hit L2 instead of queueing on HBM (+5..8%)
-    if (!sf && (lane & 15) == 0 && ne > 0)
+    if (!sf && wobs && (lane & 15) == 0 && ne > 0)
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ring_at(p, hh ? s1 : s0, wbase)),
                    "r"((uint32_t)ne * 256u) : "memory");
     uint64_t *odst = obs64 + wbase * 128 + hh * 32;
-    int cur = sf ? ne : 0;
+    int cur = (sf || !wobs) ? ne : 0;
     L.run = active && !L.halted;
     const uint4 *rp = rsrc + cur * 16;  // env `cur`'s chunk and obs row block, advanced per copy
     uint64_t *opl = odst + cur * 128;
@@ -824,7 +828,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
         L.st -= (L.st != 0u);
       }
       const int pl = (int)f + 4 - (int)p.frame_skip;  // obs plane of this frame (stack_frames)
-      if (sf && pl >= 0 && pl < 3) {
+      if (sf && wobs && pl >= 0 && pl < 3) {
         __syncwarp();
         for (int e = 0; e < ne; ++e)
           obs64[(wbase + e) * 128 + pl * 32 + lane] = sm.fb[fb_idx(warp * 32 + e, lane)];
@@ -936,19 +940,19 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
   }
-  if (obs64) {
+  if ((MODE == MODE_RESET && obs64) || (MODE != MODE_RESET && (wobs || MODE == MODE_ROLLOUT))) {
     for (int e = 0; e < ne; e += 2)
       if (e + (int)hh < ne) {
         const uint32_t el = (uint32_t)(warp * 32 + e) + hh, sw = el & kSwz;
         const uint64_t *fe = &sm.fb[el * 32u];
         uint64_t *ob = obs64 + (wbase + e + hh) * 128;
-        put_pair(fe, ob, 3u, l2, sw);
+        if (wobs) put_pair(fe, ob, 3u, l2, sw);
         if (MODE == MODE_STEP && p.frame_out)  // the newest display alone, contiguous (host frame path)
           put_pair(fe, reinterpret_cast<uint64_t *>(p.frame_out) + (wbase + e + hh) * 32, 0u, l2, sw);
         if (MODE == MODE_ROLLOUT)  // ring slot h+1: the 16-B chunk at positions l2, l2+1
           *reinterpret_cast<ulonglong2 *>(ring_at(p, (h + 1) & 3, wbase + e + hh) + l2) =
               make_ulonglong2(fe[l2], fe[l2 + 1]);
-        if (MODE == MODE_RESET || ((reset_mask >> (e + hh)) & 1u)) {
+        if (wobs && (MODE == MODE_RESET || ((reset_mask >> (e + hh)) & 1u))) {
           put_pair(fe, ob, 0u, l2, sw);
           put_pair(fe, ob, 1u, l2, sw);
           put_pair(fe, ob, 2u, l2, sw);

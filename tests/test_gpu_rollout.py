@@ -228,3 +228,25 @@ def test_rollout_config4_sampled_parity_1000_steps(game):
             assert np.array_equal(st[k], oracles[k].get_state(0)), (r, gid)
             assert np.array_equal(go[k], oo[0]) and gr[k] == orw[0] and gd[k] == od[0], (r, gid)
     assert g.stats()[0][2] == n * R * T
+
+
+def test_rollout_without_obs_keeps_history():
+    """obs_out = NULL: rewards / dones (per-step strides) and states still match the oracle, and
+    the display history stays intact, so the obs of a step right after the rollout is exact."""
+    rom, spec = workloads.game("brix_standin", max_episode_steps=11)
+    n, T = 200, 13
+    g = _env(rom, spec, n, 31)
+    o = oracle.OracleEnv(rom, spec, n, 31)
+    na = workloads.n_actions(spec)
+    acts = np.stack([workloads.gen.actions(2, k, n, na) for k in range(T)])
+    _, rew, done, term, trunc = _outs(T, n)
+    g.rollout_into(T, None, rew, done, actions=torch.from_numpy(acts).cuda(), terminated=term, truncated=trunc)
+    for k in range(T):
+        _, orw, od, ot, otr = o.step(acts[k])
+        assert np.array_equal(rew[k].cpu().numpy(), orw) and np.array_equal(done[k].cpu().numpy(), od), k
+        assert np.array_equal(term[k].cpu().numpy(), ot) and np.array_equal(trunc[k].cpu().numpy(), otr), k
+    _check_states(g, o, list(range(n)))
+    a1 = workloads.gen.actions(2, T, n, na)
+    gobs, _, _ = g.step(torch.from_numpy(a1).cuda())
+    oo, _, _, _, _ = o.step(a1)
+    assert np.array_equal(gobs.cpu().numpy().reshape(n, -1), oo)
