@@ -276,7 +276,7 @@ def time_config(rom, spec, n, steps, warmup, rank_offset, aseed, torch, OctaxEnv
 
 
 def time_rollout(rom, spec, n, T, reps, warmup_reps, rank_offset, aseed, torch, OctaxEnv, barrier=None,
-                 on_rollout=None):
+                 on_rollout=None, with_obs=True):
     """Fused rollout mode (octax_rollout, SURVEY d.8 mode "fused"): `reps` launches of T steps
     each, actions generated inside the kernel (the step mode's actions are generated before its
     timed region, so this mode does strictly more work per step), obs / reward / done written
@@ -285,7 +285,7 @@ def time_rollout(rom, spec, n, T, reps, warmup_reps, rank_offset, aseed, torch, 
     (total_ms, per-rollout ms, env)."""
     stream = torch.cuda.Stream()
     env = OctaxEnv(rom, spec, n, 0x0C7A251001764000, env_offset=rank_offset, stream=stream)
-    obs, rew, done = env.obs, env.reward, env.done
+    obs, rew, done = env.obs if with_obs else None, env.reward, env.done
     t = 0
     with torch.cuda.stream(stream):
         for _ in range(warmup_reps):
@@ -559,7 +559,16 @@ def main():
                  "ms_per_rollout_median": sorted(per_r)[len(per_r) // 2],
                  "vs_step_mode": fv / value, "stats": [int(x) for x in fst.cpu().tolist()],
                  "actions": "generated inside the rollout kernel (Philox domain 1, same stream as octax_gen_actions)",
+                 "no_obs": None,
                  "outputs": "obs / reward / done written every step (same [n] buffers as the step mode)"}
+        # the same rollouts without observations (octax_rollout obs_out = NULL: rewards / dones
+        # only, e.g. policy-free evaluation) -- the interpreter with no obs I/O, context only
+        tm, _, fenv = time_rollout(rom, spec, n, 100, R, 1, offset, workloads.ACTION_SEED, torch, OctaxEnv,
+                                   barrier, with_obs=False)
+        fenv.close()
+        tn = float(odist.max_over_ranks(torch.tensor([tm], dtype=torch.float64, device="cuda")).item())
+        fused["no_obs"] = {"steps_per_s": world * n * 100 * R / (tn / 1e3), "ms_per_step": tn / (100 * R),
+                           "note": "octax_rollout with obs_out = NULL (rewards / dones only): not the headline workload"}
         torch.cuda.empty_cache()
 
     # ---- sweep of smaller per-GPU env counts (context; parity-test configs): per-launch
