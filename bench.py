@@ -352,6 +352,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fused", action="store_true", help="skip the fused-rollout-mode measurement")
+    ap.add_argument("--no-fused-noobs", action="store_true", help="skip the observation-less fused rollouts")
     ap.add_argument("--dist-backend", default="auto", choices=["auto", "nccl", "gloo"],
                     help="auto: nccl with one GPU per rank; gloo when ranks share a device "
                          "(a functional multi-rank run on fewer GPUs than ranks)")
@@ -563,12 +564,14 @@ def main():
                  "outputs": "obs / reward / done written every step (same [n] buffers as the step mode)"}
         # the same rollouts without observations (octax_rollout obs_out = NULL: rewards / dones
         # only, e.g. policy-free evaluation) -- the interpreter with no obs I/O, context only
-        tm, _, fenv = time_rollout(rom, spec, n, 100, R, 1, offset, workloads.ACTION_SEED, torch, OctaxEnv,
-                                   barrier, with_obs=False)
-        fenv.close()
-        tn = float(odist.max_over_ranks(torch.tensor([tm], dtype=torch.float64, device="cuda")).item())
-        fused["no_obs"] = {"steps_per_s": world * n * 100 * R / (tn / 1e3), "ms_per_step": tn / (100 * R),
-                           "note": "octax_rollout with obs_out = NULL (rewards / dones only): not the headline workload"}
+        if not args.no_fused_noobs:
+            tm, _, fenv = time_rollout(rom, spec, n, 100, R, 1, offset, workloads.ACTION_SEED, torch, OctaxEnv,
+                                       barrier, with_obs=False)
+            fenv.close()
+            tn = float(odist.max_over_ranks(torch.tensor([tm], dtype=torch.float64, device="cuda")).item())
+            fused["no_obs"] = {"steps_per_s": world * n * 100 * R / (tn / 1e3), "ms_per_step": tn / (100 * R),
+                               "note": "octax_rollout with obs_out = NULL (rewards / dones only): not the "
+                                       "headline workload"}
         torch.cuda.empty_cache()
 
     # ---- sweep of smaller per-GPU env counts (context; parity-test configs): per-launch
