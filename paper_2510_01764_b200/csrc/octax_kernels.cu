@@ -790,11 +790,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     }
     if (active) {
       int32_t a = act_in;
-      if (a < 0 || (uint32_t)a >= p.n_actions) {
-        a = 0;
-        if (MODE == MODE_ROLLOUT) atomicOr(&p.s.stats[3], 1ull);  // rare: no accumulator kept live
-        else err = 1;
-      }
+      if (a < 0 || (uint32_t)a >= p.n_actions) { err = 1; a = 0; }
       set_keys(L, p.keymask[a]);
     }
     // planes 0 (lanes 0-15, ring slot s0) and 1 (lanes 16-31, slot s1) of env `cur`:
@@ -853,30 +849,13 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       term = (eval(p.term, sm, p, L, tid) != 0u) || L.halted;
       trunc = p.max_steps && steps >= p.max_steps;
       done = term | trunc;
-      if (done) {
-        if (MODE != MODE_ROLLOUT) { ret_acc += ep_ret; finished++; }
-        L.episode++;
-      }
+      if (done) { ret_acc += ep_ret; finished++; L.episode++; }
       reward[oo + env] = rew;
       done_out[oo + env] = (uint8_t)done;
       if (term_out) term_out[oo + env] = (uint8_t)term;
       if (trunc_out) trunc_out[oo + env] = (uint8_t)trunc;
     }
     resetting = active && done;
-    if (MODE == MODE_ROLLOUT) {
-      // episode statistics at the (rare) episode ends, warp-aggregated into the per-GPU int64[4]:
-      // a rollout keeps no accumulators live through its steps (register pressure in the core)
-      const uint32_t dmask = __ballot_sync(kFull, resetting);
-      if (dmask) {
-        long long r = resetting ? (long long)ep_ret : 0ll;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) r += __shfl_xor_sync(kFull, r, o);
-        if (lane == 0) {
-          atomicAdd(&p.s.stats[0], (unsigned long long)r);
-          atomicAdd(&p.s.stats[1], (unsigned long long)__popc(dmask));
-        }
-      }
-    }
     // ---- optional extras: the terminal transition's obs and the finished episode's return/length
     if (active && p.ep_ret_out) p.ep_ret_out[env] = done ? ep_ret : 0;
     if (active && p.ep_len_out) p.ep_len_out[env] = done ? steps : 0u;
