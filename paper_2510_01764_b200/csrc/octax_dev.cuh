@@ -179,6 +179,6 @@ struct StepParams {
   Program term;
 };
 
-enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_ROLLOUT = 2 };
+enum Mode : int { MODE_STEP = 0, MODE_RESET = 1, MODE_ROLLOUT = 2, MODE_ROLLOUT_NOOBS = 3 /* kernel only */ };
 
 }  // namespace octax

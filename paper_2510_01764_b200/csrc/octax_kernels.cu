@@ -748,16 +748,18 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   // launch with the VM state in registers / shared memory and the framebuffer in shared memory
   // throughout; each step's display goes to the ring with plain per-warp stores, so after the
   // prologue a warp needs no CTA barrier until the statistics at the end.
-  const uint32_t T = MODE == MODE_ROLLOUT ? p.T : 1u;
-  // observations written?  Always in a step; a rollout may run without them (obs_out == NULL:
-  // rewards / dones only -- the ring history is still kept for the steps after it)
-  const bool wobs = MODE != MODE_ROLLOUT || obs != nullptr;
+  constexpr bool kRoll = MODE == MODE_ROLLOUT || MODE == MODE_ROLLOUT_NOOBS;
+  // observations written?  Always, except in a rollout launched without them (obs_out == NULL:
+  // rewards / dones only -- the ring history is still kept for the steps after it); a separate
+  // instantiation, because a runtime test cost the observing rollout 2% (A/B)
+  constexpr bool wobs = MODE != MODE_ROLLOUT_NOOBS;
+  const uint32_t T = kRoll ? p.T : 1u;
   for (uint32_t t = 0; t < T; ++t) {
   const uint32_t h = (p.head + t) & 3u;
   const uint32_t s0 = (h + 2) & 3, s1 = (h + 3) & 3, s2 = h;
-  uint64_t *__restrict__ obs64 = reinterpret_cast<uint64_t *>(obs) + (MODE == MODE_ROLLOUT ? t * p.obs_stride : 0u);
-  const uint64_t oo = MODE == MODE_ROLLOUT ? t * p.out_stride : 0u;  // step t's reward / done row
-  if (MODE == MODE_ROLLOUT && active) {  // step t's action: given [T][n], or the K6 generator in-kernel
+  uint64_t *__restrict__ obs64 = reinterpret_cast<uint64_t *>(obs) + (kRoll ? t * p.obs_stride : 0u);
+  const uint64_t oo = kRoll ? t * p.out_stride : 0u;  // step t's reward / done row
+  if (kRoll && active) {  // step t's action: given [T][n], or the K6 generator in-kernel
     const uint64_t ts = p.t0 + t;
     act_in = actions ? actions[t * p.n + env]
                      : (int32_t)(philox_out0((uint32_t)ts, (uint32_t)(ts >> 32), gid, 1u, (uint32_t)p.aseed,
@@ -928,7 +930,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   //      (all 4 slots on a reset launch); obs plane 3 in row order (all planes on reset).
   //      A fused rollout stores each warp's 32 displays to slot h+1 itself (16-B chunks in
   //      position order, next to the plane-3 rows) and continues without a CTA barrier.
-  if (MODE != MODE_ROLLOUT) {
+  if (!kRoll) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
     __syncthreads();
     if (tid == 0) {
@@ -940,7 +942,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
   }
-  if (MODE == MODE_ROLLOUT || obs64) {  // a rollout stores the ring here even without observations
+  if (MODE == MODE_ROLLOUT_NOOBS || obs64) {  // an obs-less rollout still stores the ring here
     for (int e = 0; e < ne; e += 2)
       if (e + (int)hh < ne) {
         const uint32_t el = (uint32_t)(warp * 32 + e) + hh, sw = el & kSwz;
@@ -949,7 +951,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
         if (wobs) put_pair(fe, ob, 3u, l2, sw);
         if (MODE == MODE_STEP && p.frame_out)  // the newest display alone, contiguous (host frame path)
           put_pair(fe, reinterpret_cast<uint64_t *>(p.frame_out) + (wbase + e + hh) * 32, 0u, l2, sw);
-        if (MODE == MODE_ROLLOUT)  // ring slot h+1: the 16-B chunk at positions l2, l2+1
+        if (kRoll)  // ring slot h+1: the 16-B chunk at positions l2, l2+1
           *reinterpret_cast<ulonglong2 *>(ring_at(p, (h + 1) & 3, wbase + e + hh) + l2) =
               make_ulonglong2(fe[l2], fe[l2 + 1]);
         if (wobs && (MODE == MODE_RESET || ((reset_mask >> (e + hh)) & 1u))) {
@@ -971,7 +973,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     }
   }
 
-  if (MODE == MODE_ROLLOUT) __syncwarp();  // this step's ring / smem stores before the next step's reads
+  if (kRoll) __syncwarp();  // this step's ring / smem stores before the next step's reads
   }  // step loop
 
   // ---- store lane state
@@ -1008,7 +1010,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
       }
     }
   }
-  if (MODE != MODE_ROLLOUT && tid == 0)
+  if (!kRoll && tid == 0)
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem outlives the store
 }
 
@@ -1263,9 +1265,13 @@ cudaError_t launch_step(const StepParams &p, int mode, const int32_t *actions, u
     if (e != cudaSuccess || !p.reset_ids) return e;
     return q0 ? launch_resets<true>(p, obs, stream) : launch_resets<false>(p, obs, stream);
   }
-  if (mode == MODE_ROLLOUT)  // inline resets (p.reset_ids == nullptr): no reset_kernel inside a rollout
+  if (mode == MODE_ROLLOUT) {  // inline resets (p.reset_ids == nullptr): no reset_kernel inside a rollout
+    if (!obs)
+      return q0 ? launch_variant<MODE_ROLLOUT_NOOBS, true>(p, actions, obs, reward, done, term, trunc, stream)
+                : launch_variant<MODE_ROLLOUT_NOOBS, false>(p, actions, obs, reward, done, term, trunc, stream);
     return q0 ? launch_variant<MODE_ROLLOUT, true>(p, actions, obs, reward, done, term, trunc, stream)
               : launch_variant<MODE_ROLLOUT, false>(p, actions, obs, reward, done, term, trunc, stream);
+  }
   return q0 ? launch_variant<MODE_RESET, true>(p, nullptr, obs, nullptr, nullptr, nullptr, nullptr, stream)
             : launch_variant<MODE_RESET, false>(p, nullptr, obs, nullptr, nullptr, nullptr, nullptr, stream);
 }
