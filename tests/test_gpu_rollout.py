@@ -250,3 +250,22 @@ def test_rollout_without_obs_keeps_history():
     gobs, _, _ = g.step(torch.from_numpy(a1).cuda())
     oo, _, _, _, _ = o.step(a1)
     assert np.array_equal(gobs.cpu().numpy().reshape(n, -1), oo)
+
+
+def test_rollout_generator_high_step_index_and_zero_length():
+    """The in-kernel action generator takes the 64-bit step index t0 + t (both counter words: t0
+    past 2^32) exactly like octax_gen_actions / the oracle; T = 0 is a no-op."""
+    rom, spec = workloads.game("target_shooter_level1", max_episode_steps=19)
+    n, T, t0 = 96, 24, (1 << 32) + 5
+    g = _env(rom, spec, n, 9)
+    o = oracle.OracleEnv(rom, spec, n, 9)
+    obs, rew, done, _, _ = _outs(T, n)
+    g.rollout_into(0, obs, rew, done, aseed=77, t0=t0)  # nothing happens
+    _check_states(g, o, list(range(n)))
+    g.rollout_into(T, obs, rew, done, aseed=77, t0=t0)
+    na = workloads.n_actions(spec)
+    for k in range(T):
+        oo, orw, od, _, _ = o.step(oracle.synthetic_actions(77, t0 + k, range(n), na))
+        assert np.array_equal(obs[k].cpu().numpy().reshape(n, -1), oo), k
+        assert np.array_equal(rew[k].cpu().numpy(), orw) and np.array_equal(done[k].cpu().numpy(), od), k
+    _check_states(g, o, list(range(n)))
