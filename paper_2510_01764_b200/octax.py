@@ -233,6 +233,8 @@ class OctaxEnv:
         terminated / truncated: [T, n] or [n], likewise."""
         import torch
         n, T = self.n, int(T)
+        if T == 0:  # octax_rollout's no-op
+            return
         ob = 1024 * n
         if obs is not None and obs.numel() not in (ob, T * ob):
             raise ValueError(f"obs must hold n or T*n packed observations, got {obs.numel()} bytes")
