@@ -366,6 +366,8 @@ struct octax_env {
   float *d_reward = nullptr;
   uint8_t *d_flags = nullptr;  // done | term | trunc, 3*n
   uint8_t *d_frame = nullptr;  // [n][256] newest display (octax_step_host_frame)
+  cudaStream_t copy_stream = nullptr;           // host steps: device -> host copies of finished chunks
+  cudaEvent_t chunk_done[kMaxHostChunks] = {};  // one per chunk launch
   // get/set state staging (lazy)
   uint64_t *d_ids = nullptr;
   uint8_t *d_canon = nullptr;
@@ -385,6 +387,11 @@ static void free_env(octax_env *e) {
   cudaFree(e->d_reward);
   cudaFree(e->d_flags);
   cudaFree(e->d_frame);
+  if (e->copy_stream) {
+    cudaStreamDestroy(e->copy_stream);
+    for (auto ev : e->chunk_done)
+      if (ev) cudaEventDestroy(ev);
+  }
   cudaFree(e->d_ids);
   cudaFree(e->d_canon);
   cudaSetDevice(prev);
@@ -564,6 +571,73 @@ extern "C" octax_status octax_step_ex(octax_env *e, const int32_t *actions, void
   return OCTAX_OK;
 }
 
+// Host-buffer step, pipelined: the envs are stepped in `chunks` launches of consecutive CTA blocks
+// on the handle's stream, and each chunk's results go device -> host on a second stream as soon
+// as its launch is done, so the PCIe copy of chunk c overlaps the kernel of chunk c+1 (the copy,
+// not the kernel, bounds a host step: ~1 GB of obs vs a 0.5 ms kernel at 1M envs).  frame: copy
+// the newest display ([n][256], extras.frame_out) instead of the 4-plane obs.
+static octax_status host_step(octax_env *e, bool frame, const int32_t *actions_host, void *out_host,
+                              float *reward_host, uint8_t *done_host, uint8_t *terminated_host,
+                              uint8_t *truncated_host) {
+  DeviceGuard g(e->device);
+  const uint64_t n = e->n;
+  if (!e->d_actions) {
+    CU(cudaMalloc(&e->d_actions, 4 * n), "cudaMalloc");
+    CU(cudaMalloc(&e->d_obs, (size_t)e->obs_bytes * n), "cudaMalloc");
+    CU(cudaMalloc(&e->d_reward, 4 * n), "cudaMalloc");
+    CU(cudaMalloc(&e->d_flags, 3 * n), "cudaMalloc");
+  }
+  if (frame && !e->d_frame) CU(cudaMalloc(&e->d_frame, 256 * n), "cudaMalloc(frame)");
+  if (!e->copy_stream) {
+    CU(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking), "copy stream");
+    for (auto &ev : e->chunk_done) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+  }
+  CU(cudaMemcpyAsync(e->d_actions, actions_host, 4 * n, cudaMemcpyHostToDevice, e->stream), "H2D actions");
+  const uint32_t nblocks = (uint32_t)((n + kBlock - 1) / kBlock);
+  // chunks: a launch per ~one wave of CTAs (148 SMs x 5), at most kMaxHostChunks: the first
+  // chunk's kernel is the only compute not hidden behind a copy
+  uint32_t chunks = nblocks / 740u;
+  chunks = chunks < 1u ? 1u : (chunks > kMaxHostChunks ? kMaxHostChunks : chunks);
+  uint8_t *packed = e->obs_format == OCTAX_OBS_PACKED ? e->d_obs : e->packed_scratch;
+  const size_t ob = e->obs_bytes;
+  for (uint32_t c = 0; c < chunks; ++c) {
+    const uint32_t b0 = (uint32_t)((uint64_t)nblocks * c / chunks), b1 = (uint32_t)((uint64_t)nblocks * (c + 1) / chunks);
+    const uint64_t e0 = (uint64_t)b0 * kBlock, e1 = (uint64_t)b1 * kBlock < n ? (uint64_t)b1 * kBlock : n;
+    StepParams p = e->p;
+    p.final_obs = nullptr;
+    p.frame_out = frame ? e->d_frame : nullptr;
+    p.ep_ret_out = nullptr;
+    p.ep_len_out = nullptr;
+    p.block_base = b0;
+    p.block_count = b1 - b0;
+    CU(launch_step(p, MODE_STEP, e->d_actions, packed, e->d_reward, e->d_flags, e->d_flags + n, e->d_flags + 2 * n,
+                   e->stream), "step kernel");
+    if (e->obs_format != OCTAX_OBS_PACKED && !frame)
+      CU(launch_expand_obs(e1 - e0, packed + e0 * 1024, e->d_obs + e0 * ob, e->stream), "expand obs");
+    CU(cudaEventRecord(e->chunk_done[c], e->stream), "event record");
+    CU(cudaStreamWaitEvent(e->copy_stream, e->chunk_done[c], 0), "stream wait");
+    const uint64_t m = e1 - e0;
+    if (frame)
+      CU(cudaMemcpyAsync((uint8_t *)out_host + e0 * 256, e->d_frame + e0 * 256, 256 * m, cudaMemcpyDeviceToHost,
+                         e->copy_stream), "D2H frame");
+    else
+      CU(cudaMemcpyAsync((uint8_t *)out_host + e0 * ob, e->d_obs + e0 * ob, ob * m, cudaMemcpyDeviceToHost,
+                         e->copy_stream), "D2H obs");
+    CU(cudaMemcpyAsync(reward_host + e0, e->d_reward + e0, 4 * m, cudaMemcpyDeviceToHost, e->copy_stream), "D2H reward");
+    CU(cudaMemcpyAsync(done_host + e0, e->d_flags + e0, m, cudaMemcpyDeviceToHost, e->copy_stream), "D2H done");
+    if (terminated_host)
+      CU(cudaMemcpyAsync(terminated_host + e0, e->d_flags + n + e0, m, cudaMemcpyDeviceToHost, e->copy_stream),
+         "D2H term");
+    if (truncated_host)
+      CU(cudaMemcpyAsync(truncated_host + e0, e->d_flags + 2 * n + e0, m, cudaMemcpyDeviceToHost, e->copy_stream),
+         "D2H trunc");
+  }
+  e->p.head = (e->p.head + 1) & 3u;
+  CU(cudaStreamSynchronize(e->copy_stream), "sync");
+  CU(cudaStreamSynchronize(e->stream), "sync");
+  return OCTAX_OK;
+}
+
 extern "C" octax_status octax_step(octax_env *e, const int32_t *actions, void *obs_out, float *reward_out,
                                    uint8_t *done_out, uint8_t *terminated_out, uint8_t *truncated_out) {
   return octax_step_ex(e, actions, obs_out, reward_out, done_out, terminated_out, truncated_out, nullptr);
@@ -574,26 +648,15 @@ extern "C" octax_status octax_step_host(octax_env *e, const int32_t *actions_hos
                                         uint8_t *truncated_host) {
   if (!e || !actions_host || !obs_host || !reward_host || !done_host)
     return set_err(OCTAX_E_INVALID_ARG, "NULL argument to octax_step_host");
-  DeviceGuard g(e->device);
-  const uint64_t n = e->n;
-  if (!e->d_actions) {
-    CU(cudaMalloc(&e->d_actions, 4 * n), "cudaMalloc");
-    CU(cudaMalloc(&e->d_obs, (size_t)e->obs_bytes * n), "cudaMalloc");
-    CU(cudaMalloc(&e->d_reward, 4 * n), "cudaMalloc");
-    CU(cudaMalloc(&e->d_flags, 3 * n), "cudaMalloc");
-  }
-  CU(cudaMemcpyAsync(e->d_actions, actions_host, 4 * n, cudaMemcpyHostToDevice, e->stream), "H2D actions");
-  octax_status st = octax_step(e, e->d_actions, e->d_obs, e->d_reward, e->d_flags, e->d_flags + n, e->d_flags + 2 * n);
-  if (st != OCTAX_OK) return st;
-  CU(cudaMemcpyAsync(obs_host, e->d_obs, (size_t)e->obs_bytes * n, cudaMemcpyDeviceToHost, e->stream), "D2H obs");
-  CU(cudaMemcpyAsync(reward_host, e->d_reward, 4 * n, cudaMemcpyDeviceToHost, e->stream), "D2H reward");
-  CU(cudaMemcpyAsync(done_host, e->d_flags, n, cudaMemcpyDeviceToHost, e->stream), "D2H done");
-  if (terminated_host)
-    CU(cudaMemcpyAsync(terminated_host, e->d_flags + n, n, cudaMemcpyDeviceToHost, e->stream), "D2H term");
-  if (truncated_host)
-    CU(cudaMemcpyAsync(truncated_host, e->d_flags + 2 * n, n, cudaMemcpyDeviceToHost, e->stream), "D2H trunc");
-  CU(cudaStreamSynchronize(e->stream), "sync");
-  return OCTAX_OK;
+  return host_step(e, false, actions_host, obs_host, reward_host, done_host, terminated_host, truncated_host);
+}
+
+extern "C" octax_status octax_step_host_frame(octax_env *e, const int32_t *actions_host, void *frame_host,
+                                              float *reward_host, uint8_t *done_host, uint8_t *terminated_host,
+                                              uint8_t *truncated_host) {
+  if (!e || !actions_host || !frame_host || !reward_host || !done_host)
+    return set_err(OCTAX_E_INVALID_ARG, "NULL argument to octax_step_host_frame");
+  return host_step(e, true, actions_host, frame_host, reward_host, done_host, terminated_host, truncated_host);
 }
 
 extern "C" octax_status octax_rollout(octax_env *e, uint32_t T, const int32_t *actions, uint64_t aseed, uint64_t t0,
@@ -627,36 +690,6 @@ extern "C" octax_status octax_rollout(octax_env *e, uint32_t T, const int32_t *a
                  e->stream),
      "rollout kernel");
   e->p.head = (e->p.head + T) & 3u;
-  return OCTAX_OK;
-}
-
-extern "C" octax_status octax_step_host_frame(octax_env *e, const int32_t *actions_host, void *frame_host,
-                                              float *reward_host, uint8_t *done_host, uint8_t *terminated_host,
-                                              uint8_t *truncated_host) {
-  if (!e || !actions_host || !frame_host || !reward_host || !done_host)
-    return set_err(OCTAX_E_INVALID_ARG, "NULL argument to octax_step_host_frame");
-  DeviceGuard g(e->device);
-  const uint64_t n = e->n;
-  if (!e->d_actions) {
-    CU(cudaMalloc(&e->d_actions, 4 * n), "cudaMalloc");
-    CU(cudaMalloc(&e->d_obs, (size_t)e->obs_bytes * n), "cudaMalloc");
-    CU(cudaMalloc(&e->d_reward, 4 * n), "cudaMalloc");
-    CU(cudaMalloc(&e->d_flags, 3 * n), "cudaMalloc");
-  }
-  if (!e->d_frame) CU(cudaMalloc(&e->d_frame, 256 * n), "cudaMalloc(frame)");
-  CU(cudaMemcpyAsync(e->d_actions, actions_host, 4 * n, cudaMemcpyHostToDevice, e->stream), "H2D actions");
-  octax_step_extras ex = {nullptr, nullptr, nullptr, e->d_frame};
-  octax_status st = octax_step_ex(e, e->d_actions, e->d_obs, e->d_reward, e->d_flags, e->d_flags + n,
-                                  e->d_flags + 2 * n, &ex);
-  if (st != OCTAX_OK) return st;
-  CU(cudaMemcpyAsync(frame_host, e->d_frame, 256 * n, cudaMemcpyDeviceToHost, e->stream), "D2H frame");
-  CU(cudaMemcpyAsync(reward_host, e->d_reward, 4 * n, cudaMemcpyDeviceToHost, e->stream), "D2H reward");
-  CU(cudaMemcpyAsync(done_host, e->d_flags, n, cudaMemcpyDeviceToHost, e->stream), "D2H done");
-  if (terminated_host)
-    CU(cudaMemcpyAsync(terminated_host, e->d_flags + n, n, cudaMemcpyDeviceToHost, e->stream), "D2H term");
-  if (truncated_host)
-    CU(cudaMemcpyAsync(truncated_host, e->d_flags + 2 * n, n, cudaMemcpyDeviceToHost, e->stream), "D2H trunc");
-  CU(cudaStreamSynchronize(e->stream), "sync");
   return OCTAX_OK;
 }
 

@@ -14,6 +14,7 @@ namespace octax {
 constexpr int kBlock = OCTAX_BLOCK;  // envs (threads) per CTA (a multiple of 32)
 constexpr int kMinBlocks = OCTAX_MINB;  // resident CTAs per SM the step kernel is built for
 constexpr int kMaxStartup = 32;
+constexpr uint32_t kMaxHostChunks = 8;  // pipelined host steps: launches per step (octax_api.cpp host_step)
 constexpr int kMaxOps = 64;
 constexpr int kMaxDepth = 8;
 constexpr uint32_t kImageBytes = 4096;
@@ -153,6 +154,8 @@ struct StepParams {
   uint32_t *reset_ids;     // [n] env ids appended by the step kernel, run by reset_kernel
   uint64_t n;
   uint64_t env_offset;
+  uint32_t block_base;    // first CTA block of this launch (a chunk of the envs, host paths)
+  uint32_t block_count;   // CTA blocks in this launch; 0 = all blocks from block_base
   uint64_t seed;
   uint32_t head;          // ring slot holding the current display
   uint32_t frame_skip;

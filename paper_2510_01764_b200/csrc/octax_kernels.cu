@@ -693,7 +693,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
   extern __shared__ __align__(128) unsigned char smraw[];
   Smem &sm = *reinterpret_cast<Smem *>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t block0 = (uint64_t)blockIdx.x * kBlock;
+  const uint64_t block0 = ((uint64_t)blockIdx.x + p.block_base) * kBlock;
   const uint64_t env = block0 + tid;
   const uint32_t nlive = p.n - block0 < (uint64_t)kBlock ? (uint32_t)(p.n - block0) : (uint32_t)kBlock;
   const bool active = (uint32_t)tid < nlive;  // (32-bit: cheap to rematerialise)
@@ -1227,7 +1227,7 @@ static cudaError_t launch_variant(const StepParams &p, const int32_t *actions, u
     if (e != cudaSuccess) return e;
     attr_set.fetch_or(bit, std::memory_order_relaxed);
   }
-  const unsigned grid = (unsigned)((p.n + kBlock - 1) / kBlock);
+  const unsigned grid = p.block_count ? p.block_count : (unsigned)((p.n + kBlock - 1) / kBlock - p.block_base);
   octax_kernel<MODE, Q0><<<grid, kBlock, smem, stream>>>(p, actions, obs, reward, done, term, trunc);
   return cudaGetLastError();
 }

@@ -783,3 +783,39 @@ def test_gymnax_env_matches_oracle():
     with pytest.raises(ValueError):
         env.step(None, old, torch.from_numpy(a))
     env.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("startup", [None, [(1 << 1, 2)]])
+def test_pipelined_host_steps_match_device_steps(startup):
+    """octax_step_host / octax_step_host_frame at 262,144 envs step the envs in several chunk
+    launches whose device->host copies overlap the next chunk's kernel: outputs equal a twin
+    handle stepped with octax_step on the device, step by step, including synchronized
+    truncations (deferred resets per chunk when the spec has startup segments)."""
+    from paper_2510_01764_b200 import OctaxEnv
+    over = dict(max_episode_steps=3)
+    if startup:
+        over["startup"] = startup
+    rom, spec = workloads.game("brix_standin", **over)
+    n = 262144
+    host_full, host_frame, dev = (OctaxEnv(rom, spec, n, 5) for _ in range(3))
+    na = workloads.n_actions(spec)
+    o_h = np.zeros((n, 1024), np.uint8)
+    f_h = np.zeros((n, 32, 8), np.uint8)
+    r1, r2 = np.zeros(n, np.float32), np.zeros(n, np.float32)
+    d1, d2 = np.zeros(n, np.uint8), np.zeros(n, np.uint8)
+    t1, t2 = np.zeros(n, np.uint8), np.zeros(n, np.uint8)
+    for t in range(7):
+        a = np.ascontiguousarray(workloads.gen.actions(3, t, n, na))
+        host_full.step_host(a, o_h, r1, d1, t1)
+        host_frame.step_host_frame(a, f_h, r2, d2, t2)
+        obs, rew, done = dev.step(torch.from_numpy(a).cuda())
+        ob = obs.cpu().numpy().reshape(n, 1024)
+        assert np.array_equal(o_h, ob), t
+        assert np.array_equal(f_h.reshape(n, 256), ob[:, 768:]), t
+        rw, dn, tm = rew.cpu().numpy(), done.cpu().numpy(), dev.terminated.cpu().numpy()
+        for r_, d_, t_ in ((r1, d1, t1), (r2, d2, t2)):
+            assert np.array_equal(r_, rw) and np.array_equal(d_, dn) and np.array_equal(t_, tm), t
+    assert d1.sum() > 0 or dev.stats()[0][1] > 0
+    for e in (host_full, host_frame, dev):
+        assert np.array_equal(e.state_digests()[0][:4096], dev.state_digests()[0][:4096])
