@@ -170,9 +170,12 @@ octax_status octax_step_ex(octax_env *e, const int32_t *actions, void *obs_out, 
                            uint8_t *done_out, uint8_t *terminated_out, uint8_t *truncated_out,
                            const octax_step_extras *extras);
 
-/* Same step with HOST buffers (pinned recommended): copies actions host->device,
- * runs octax_step on internal device buffers, copies obs/reward/done back and
- * synchronises.  terminated_out / truncated_out may be NULL. */
+/* Same step with HOST buffers (pinned recommended): copies actions host->device, steps the envs
+ * on internal device buffers, copies obs/reward/done back and synchronises.  terminated_out /
+ * truncated_out may be NULL.  Large batches are stepped in several launches over consecutive
+ * env blocks; each block's results are copied back on a second stream while the next block's
+ * launch runs (the PCIe copy, not the kernel, bounds a host step).  Results are identical to
+ * octax_step. */
 octax_status octax_step_host(octax_env *e, const int32_t *actions_host, void *obs_host,
                              float *reward_host, uint8_t *done_host, uint8_t *terminated_host,
                              uint8_t *truncated_host);
