@@ -594,8 +594,9 @@ static octax_status host_step(octax_env *e, bool frame, const int32_t *actions_h
   }
   CU(cudaMemcpyAsync(e->d_actions, actions_host, 4 * n, cudaMemcpyHostToDevice, e->stream), "H2D actions");
   const uint32_t nblocks = (uint32_t)((n + kBlock - 1) / kBlock);
-  // chunks: a launch per ~one wave of CTAs (148 SMs x 5), at most kMaxHostChunks: the first
-  // chunk's kernel is the only compute not hidden behind a copy
+  // chunks: a launch per >= one wave of CTAs (148 SMs x 5), at most kMaxHostChunks: the first
+  // chunk's kernel is the only compute not hidden behind a copy (A/B at 1M envs: 1 chunk 1.73e8,
+  // 2 chunks 1.93e8, 5 chunks 2.02e8 env steps/s through octax_step_host_frame)
   uint32_t chunks = nblocks / 740u;
   chunks = chunks < 1u ? 1u : (chunks > kMaxHostChunks ? kMaxHostChunks : chunks);
   uint8_t *packed = e->obs_format == OCTAX_OBS_PACKED ? e->d_obs : e->packed_scratch;
@@ -623,15 +624,15 @@ static octax_status host_step(octax_env *e, bool frame, const int32_t *actions_h
     else
       CU(cudaMemcpyAsync((uint8_t *)out_host + e0 * ob, e->d_obs + e0 * ob, ob * m, cudaMemcpyDeviceToHost,
                          e->copy_stream), "D2H obs");
-    CU(cudaMemcpyAsync(reward_host + e0, e->d_reward + e0, 4 * m, cudaMemcpyDeviceToHost, e->copy_stream), "D2H reward");
-    CU(cudaMemcpyAsync(done_host + e0, e->d_flags + e0, m, cudaMemcpyDeviceToHost, e->copy_stream), "D2H done");
-    if (terminated_host)
-      CU(cudaMemcpyAsync(terminated_host + e0, e->d_flags + n + e0, m, cudaMemcpyDeviceToHost, e->copy_stream),
-         "D2H term");
-    if (truncated_host)
-      CU(cudaMemcpyAsync(truncated_host + e0, e->d_flags + 2 * n + e0, m, cudaMemcpyDeviceToHost, e->copy_stream),
-         "D2H trunc");
   }
+  // the small per-env outputs (5 B/env) once, after the last chunk: per-copy overhead, not bytes,
+  // is their cost
+  CU(cudaMemcpyAsync(reward_host, e->d_reward, 4 * n, cudaMemcpyDeviceToHost, e->copy_stream), "D2H reward");
+  CU(cudaMemcpyAsync(done_host, e->d_flags, n, cudaMemcpyDeviceToHost, e->copy_stream), "D2H done");
+  if (terminated_host)
+    CU(cudaMemcpyAsync(terminated_host, e->d_flags + n, n, cudaMemcpyDeviceToHost, e->copy_stream), "D2H term");
+  if (truncated_host)
+    CU(cudaMemcpyAsync(truncated_host, e->d_flags + 2 * n, n, cudaMemcpyDeviceToHost, e->copy_stream), "D2H trunc");
   e->p.head = (e->p.head + 1) & 3u;
   CU(cudaStreamSynchronize(e->copy_stream), "sync");
   CU(cudaStreamSynchronize(e->stream), "sync");

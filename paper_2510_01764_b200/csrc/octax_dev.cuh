@@ -14,7 +14,10 @@ namespace octax {
 constexpr int kBlock = OCTAX_BLOCK;  // envs (threads) per CTA (a multiple of 32)
 constexpr int kMinBlocks = OCTAX_MINB;  // resident CTAs per SM the step kernel is built for
 constexpr int kMaxStartup = 32;
-constexpr uint32_t kMaxHostChunks = 8;  // pipelined host steps: launches per step (octax_api.cpp host_step)
+#ifndef OCTAX_HOST_CHUNKS
+#define OCTAX_HOST_CHUNKS 8
+#endif
+constexpr uint32_t kMaxHostChunks = OCTAX_HOST_CHUNKS;  // pipelined host steps: launches per step (octax_api.cpp host_step)
 constexpr int kMaxOps = 64;
 constexpr int kMaxDepth = 8;
 constexpr uint32_t kImageBytes = 4096;
