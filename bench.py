@@ -311,6 +311,22 @@ def time_rollout(rom, spec, n, T, reps, warmup_reps, rank_offset, aseed, torch, 
     return ev[0].elapsed_time(ev[reps]), per, env
 
 
+def fused_model(game, n):
+    """ncu counts of one fused rollout launch (profiles/latest_fused_full.json, per env step) if
+    the capture is of this build (device-code digest), game and env count."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "latest_fused_full.json")) as f:
+            j = json.load(f)
+        from paper_2510_01764_b200 import octax
+        from paper_2510_01764_b200.build import device_code_digest
+        if (j.get("sass_sha256") == device_code_digest(octax.SO_PATH) and j.get("game") == game
+                and "octax_kernel<2," in str(j.get("kernel_symbol", "")) and j.get("envs_per_launch") == n):
+            return j
+    except Exception:
+        pass
+    return None
+
+
 def issue_model(game, n):
     """ncu instruction counts of the step kernel (profiles/latest_step_full.json), used for the
     ALU-pipe and issue roofs only if the profile is of THIS build and workload: the device-code
@@ -551,10 +567,17 @@ def main():
         hbm_f = f_bytes * fv / world / 1e9
         fused_roof = {"hbm": {"achieved": hbm_f, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_f / hbm_peak,
                               "alg_bytes_per_env_step": f_bytes}}
-        if alu:
+        fm = fused_model(args.game, n)
+        if fm and fm.get("alu_warp_instr_per_env_step"):
+            a_f = fm["alu_warp_instr_per_env_step"] * 32 * fv / world / 1e9
+            peak_alu = 148 * 4 * 0.5 * 32 * f_sm / 1e9
+            fused_roof["alu"] = {"achieved": a_f, "peak": peak_alu, "frac": a_f / peak_alu,
+                                 "alu_warp_instr_per_env_step": fm["alu_warp_instr_per_env_step"],
+                                 "source": "profiles/latest_fused_full.json (ncu of one rollout launch of this build)"}
+        elif alu:
             a_f = alu["alu_warp_instr_per_env_step"] * 32 * fv / world / 1e9
             fused_roof["alu"] = {"achieved": a_f, "peak": alu["peak"], "frac": a_f / alu["peak"],
-                                 "note": "step kernel's ALU-pipe instructions per env step (upper bound)"}
+                                 "note": "step kernel's ALU-pipe instructions per env step (no fused capture of this build)"}
         fused = {"mode": "fused", "steps_per_rollout": 100, "rollouts_timed": R, "warmup_rollouts": 1,
                  "steps_per_s": fv, "frames_per_s": 4 * fv, "ms_per_step": tf / (100 * R), "roofline": fused_roof,
                  "ms_per_rollout_median": sorted(per_r)[len(per_r) // 2],

@@ -35,7 +35,8 @@ if [ -n "$FUSED_NCU" ]; then  # one 100-step fused rollout launch (octax_kernel<
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:octax_kernel -s 8 -c 1 \
     -o gpurun_out/fused_1048576 -f $PCMD > gpurun_out/ncu_fused.log 2>&1; echo "ncu fused rc=$?"
   python scripts/ncu_summary.py full gpurun_out/fused_1048576.ncu-rep gpurun_out/fused_full_1048576.json \
-    --envs 104857600 --game pong_standin --so $SO > /dev/null 2>&1
+    --envs 104857600 --game pong_standin --envs_per_launch 1048576 --so $SO > /dev/null 2>&1 && \
+    cp gpurun_out/fused_full_1048576.json profiles/latest_fused_full.json
 fi
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 if [ -n "$LAUNCHES" ]; then
