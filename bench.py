@@ -478,6 +478,12 @@ def main():
 
     # issue roof (SURVEY d.2): 148 SMs x 4 schedulers x 1 warp instruction per cycle x f_SM,
     # against all warp instructions per env step measured by ncu (same source as the ALU count)
+    # SURVEY d.2's a-priori issue roof (I_step ~ 2,000 thread instructions per env step, estimated
+    # before any kernel existed): context for the self-referential measured-instruction roofs
+    survey_issue = {"I_step_thread_estimate": 2000, "roof_env_steps_per_s": 148 * 4 * 32 * f_sm / 2000,
+                    "frac": value / world / (148 * 4 * 32 * f_sm / 2000),
+                    "I_step_thread_measured": (im["warp_instr_per_env_step"] * 32 * im.get("warp_exec_efficiency", 1.0)
+                                               if im and im.get("warp_instr_per_env_step") else None)}
     issue = None
     if im and im.get("warp_instr_per_env_step"):
         peak_iss = 148 * 4 * f_sm / 1e9
@@ -671,7 +677,7 @@ def main():
                               if world > ndev else "one GPU per rank")},
             "roofline": ({"bound": "alu", "achieved": alu["achieved"], "peak": alu["peak"], "unit": alu["unit"],
                           "frac": alu["frac"], "traffic": traffic, "kernel": "octax_kernel<MODE_STEP>",
-                          "kernel_ms_median": kernel_ms, "alu": alu, "issue": issue,
+                          "kernel_ms_median": kernel_ms, "alu": alu, "issue": issue, "issue_survey_estimate": survey_issue,
                           "hbm": {"achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                                   "alg_bytes_per_env_step": ALG_BYTES_PER_ENV_STEP, "peak_source": peak_src,
                                   "roof_env_steps_per_s": hbm_peak * 1e9 / ALG_BYTES_PER_ENV_STEP}}
