@@ -50,7 +50,14 @@
 namespace octax {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr uint32_t kLaneDrawMax = 8;  // rows: lane-parallel DXYN up to this, cooperative above
+#ifndef OCTAX_LANE_DRAW_MAX
+#define OCTAX_LANE_DRAW_MAX 8
+#endif
+#ifndef OCTAX_GROUP_MIN_ROWS
+#define OCTAX_GROUP_MIN_ROWS 3
+#endif
+constexpr uint32_t kLaneDrawMax = OCTAX_LANE_DRAW_MAX;  // rows: lane-parallel DXYN up to this, cooperative above
+constexpr uint32_t kGroupMinRows = OCTAX_GROUP_MIN_ROWS;  // grouped DXYN from this many rows (A/B knobs)
 // ceil(2^32 / m): lane / m = umulhi(lane, kRecip[m]) exactly for lane < 2^16 (m = 2..15)
 __constant__ uint32_t kRecip[16] = {0u, 0u, 0x80000000u, 0x55555556u, 0x40000000u, 0x33333334u,
                                     0x2AAAAAABu, 0x24924925u, 0x20000000u, 0x1C71C71Du, 0x1999999Au,
@@ -595,7 +602,7 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
     const uint32_t dm = __ballot_sync(kFull, nrows != 0u);
     // one grouped pass (groups of maxr lanes, 32 / maxr drawers) when the drawers fit and
     // rows are many enough to beat maxr lane-parallel row steps (uniform choice)
-    if (maxr >= 3u && (uint32_t)__popc(dm) * maxr <= 32u)  // k drawers fit 32 / maxr groups
+    if (maxr >= kGroupMinRows && (uint32_t)__popc(dm) * maxr <= 32u)  // k drawers fit 32 / maxr groups
     {
       if (wdirty)
         draw_groups<true, SCAT>(sm, L, p, tid, lane, block0, dm, vx & 63u, y0, L.I & 0xFFFu, nrows, maxr, wdirty, quirks, do_draw);
