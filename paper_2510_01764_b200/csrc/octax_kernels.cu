@@ -58,6 +58,7 @@ constexpr unsigned kFull = 0xffffffffu;
 #endif
 constexpr uint32_t kLaneDrawMax = OCTAX_LANE_DRAW_MAX;  // rows: lane-parallel DXYN up to this, cooperative above
 constexpr uint32_t kGroupMinRows = OCTAX_GROUP_MIN_ROWS;  // grouped DXYN from this many rows (A/B knobs)
+static_assert(kLaneDrawMax <= 8u, "the lane-parallel fast path realigns an 8-byte sprite window");
 // ceil(2^32 / m): lane / m = umulhi(lane, kRecip[m]) exactly for lane < 2^16 (m = 2..15)
 __constant__ uint32_t kRecip[16] = {0u, 0u, 0x80000000u, 0x55555556u, 0x40000000u, 0x33333334u,
                                     0x2AAAAAABu, 0x24924925u, 0x20000000u, 0x1C71C71Du, 0x1999999Au,
