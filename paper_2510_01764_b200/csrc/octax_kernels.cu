@@ -735,17 +735,8 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
     L.sp = c.y & 255u; L.dt = (c.y >> 8) & 255u; L.st = (c.y >> 16) & 255u; L.halted = c.y >> 24;
     if (L.halted) L.pc |= 0x10000u;
     L.draw = c.z; L.episode = c.w;
-#ifdef OCTAX_LATE_BOOK
-    if (MODE == MODE_STEP) {  // read after the frame loop: three registers fewer through it
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(p.s.book + env));
-    } else {
-      uint4 b = p.s.book[env];
-      steps = b.x; prev = b.y; ep_ret = (int32_t)b.z;
-    }
-#else
     uint4 b = p.s.book[env];
     steps = b.x; prev = b.y; ep_ret = (int32_t)b.z;
-#endif
     uint4 s0 = p.s.stack[env * 2], s1 = p.s.stack[env * 2 + 1];
     uint32_t sw[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
@@ -863,12 +854,6 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
 #pragma unroll 4
     for (int e = cur; e < ne; ++e, rp += 16, opl += 128) put_rows(opl, 0u, l2 ^ ((uint32_t)e & kSwz), __ldcs(rp));
     if (active) L.halted = !L.run;
-#ifdef OCTAX_LATE_BOOK
-    if (MODE == MODE_STEP && active) {
-      const uint4 b = p.s.book[env];
-      steps = b.x; prev = b.y; ep_ret = (int32_t)b.z;
-    }
-#endif
     if (active) {
       const uint32_t s = eval(p.score, sm, p, L, tid);
       const int32_t d = (int32_t)(s - prev);
