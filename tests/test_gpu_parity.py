@@ -819,3 +819,36 @@ def test_pipelined_host_steps_match_device_steps(startup):
     assert d1.sum() > 0 or dev.stats()[0][1] > 0
     for e in (host_full, host_frame, dev):
         assert np.array_equal(e.state_digests()[0][:4096], dev.state_digests()[0][:4096])
+
+
+@pytest.mark.slow
+def test_max_size_16M_envs_sampled_parity():
+    """Maximum sizes: 16,777,293 envs (2^24 + 77, a ragged last CTA) on one B200 -- ~87 GB of VM
+    state plus 17 GB of packed obs, byte offsets far past 2^32 in every per-env array.  Three steps
+    (one of them a fused rollout of two steps) with device-generated actions; envs near the ends of
+    the range and around 2^24 are compared with the oracle in full canonical state and outputs."""
+    rom, spec = workloads.game("brix_standin", max_episode_steps=2)
+    n = (1 << 24) + 77
+    g = _gpu_env(rom, spec, n, workloads.ENV_SEED)
+    ids = [0, 1, 127, 128, (1 << 23) + 5, (1 << 24) - 1, 1 << 24, n - 2, n - 1]
+    oracles = [oracle.OracleEnv(rom, spec, 1, workloads.ENV_SEED, gid) for gid in ids]
+    na = workloads.n_actions(spec)
+    a = torch.empty(n, dtype=torch.int32, device="cuda")
+    idx = torch.tensor(ids, device="cuda")
+    g.gen_actions(workloads.ACTION_SEED, 0, a)
+    obs, rew, done = g.step(a)
+    go, gr, gd = obs.reshape(n, -1)[idx].cpu().numpy(), rew[idx].cpu().numpy(), done[idx].cpu().numpy()
+    for k, gid in enumerate(ids):
+        oo, orw, od, _, _ = oracles[k].step(np.array([oracle.synthetic_action(workloads.ACTION_SEED, 0, gid, na)], np.int32))
+        assert np.array_equal(go[k], oo[0]) and gr[k] == orw[0] and gd[k] == od[0], gid
+    g.rollout_into(2, g.obs, g.reward, g.done, aseed=workloads.ACTION_SEED, t0=1)
+    for k, gid in enumerate(ids):
+        for t in (1, 2):
+            oo, orw, od, _, _ = oracles[k].step(np.array([oracle.synthetic_action(workloads.ACTION_SEED, t, gid, na)], np.int32))
+    go, gr, gd = g.obs.reshape(n, -1)[idx].cpu().numpy(), g.reward[idx].cpu().numpy(), g.done[idx].cpu().numpy()
+    st = g.get_states(ids)
+    for k, gid in enumerate(ids):
+        assert np.array_equal(st[k], oracles[k].get_state(0)), gid
+    s, _ = g.stats()
+    assert s[2] == 3 * n and s[1] >= n  # every env truncated at step 2 (max_episode_steps = 2)
+    g.close()
