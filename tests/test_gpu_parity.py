@@ -842,12 +842,12 @@ def test_max_size_16M_envs_sampled_parity():
         oo, orw, od, _, _ = oracles[k].step(np.array([oracle.synthetic_action(workloads.ACTION_SEED, 0, gid, na)], np.int32))
         assert np.array_equal(go[k], oo[0]) and gr[k] == orw[0] and gd[k] == od[0], gid
     g.rollout_into(2, g.obs, g.reward, g.done, aseed=workloads.ACTION_SEED, t0=1)
-    for k, gid in enumerate(ids):
-        for t in (1, 2):
-            oo, orw, od, _, _ = oracles[k].step(np.array([oracle.synthetic_action(workloads.ACTION_SEED, t, gid, na)], np.int32))
     go, gr, gd = g.obs.reshape(n, -1)[idx].cpu().numpy(), g.reward[idx].cpu().numpy(), g.done[idx].cpu().numpy()
     st = g.get_states(ids)
     for k, gid in enumerate(ids):
+        for t in (1, 2):
+            oo, orw, od, _, _ = oracles[k].step(np.array([oracle.synthetic_action(workloads.ACTION_SEED, t, gid, na)], np.int32))
+        assert np.array_equal(go[k], oo[0]) and gr[k] == orw[0] and gd[k] == od[0], gid
         assert np.array_equal(st[k], oracles[k].get_state(0)), gid
     s, _ = g.stats()
     assert s[2] == 3 * n and s[1] >= n  # every env truncated at step 2 (max_episode_steps = 2)
