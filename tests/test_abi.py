@@ -93,3 +93,20 @@ def test_gymnax_key_to_seed():
     assert seed_from_key([0x12345678, 0x9ABCDEF0]) == 0x123456789ABCDEF0
     with pytest.raises(ValueError):
         seed_from_key([1, 2, 3])
+
+
+def test_create_rejects_empty_and_oversized_batches(lib):
+    """n_envs = 0 and n_envs > 2^31 are refused on the host, before any device allocation."""
+    cs, keep = _spec()
+    rom = (ctypes.c_uint8 * 2)(0x12, 0x00)
+    for n in (0, (1 << 31) + 1):
+        h = ctypes.c_void_p()
+        assert lib.octax_create(rom, 2, ctypes.byref(cs), n, 1, None, ctypes.byref(h)) == -1
+        assert h.value is None and "n_envs" in lib.octax_last_error().decode()
+
+
+def test_null_arguments_new_entry_points(lib):
+    """octax_rollout / octax_step_host_frame / octax_step_host refuse NULL handles and buffers."""
+    assert lib.octax_rollout(None, 4, None, 0, 0, None, 0, None, None, None, None, 0) == -1
+    assert lib.octax_step_host_frame(None, None, None, None, None, None, None) == -1
+    assert lib.octax_step_host(None, None, None, None, None, None, None) == -1
