@@ -173,6 +173,43 @@ def regroup(game, warm=300, steps=24, cta=128):
                 "pc_uniform": v["pc_uni"] / wc, "class_uniform": v["cls_uni"] / wc} for g, v in score.items()}
 
 
+def sleepers(game, warm=300, steps=24, cta=128):
+    """SURVEY NEXT-2 (ii) with (i): the frames an env sleeps through entirely -- halted, a
+    self-jump, or a delay-poll loop (FX07; 3X00; 1NNN) entered with DT > 0 at the frame start (DT
+    only changes at the frame's end, so the env provably loops until then) -- and how many whole
+    warps a per-frame regrouping of a 128-env CTA by that status could skip: floor(sleepers / 32)
+    per CTA-frame, against identity grouping (a warp skips only if all its 32 envs sleep)."""
+    rom, spec = workloads.game(game)
+    ipf, fs = spec["instructions_per_frame"], spec["frame_skip"]
+    o = oracle.OracleEnv(rom, spec, cta, workloads.ENV_SEED)
+    na = workloads.n_actions(spec)
+    mem0 = [int(v) for v in oracle.canon_fields(o.get_state(0))["mem"]] + [0] * 8
+    loops = _poll_loops(mem0)
+    for t in range(warm):
+        o.step(workloads.gen.actions(workloads.ACTION_SEED, t, cta, na))
+    lane_frames = sleeping = warp_frames = skip_regroup = skip_ident = 0
+    for t in range(warm, warm + steps):
+        a = workloads.gen.actions(workloads.ACTION_SEED, t, cta, na)
+        keys = [0 if x == 0 else 1 << spec["action_keys"][x - 1] for x in a]
+        for _ in range(fs):
+            sl = []
+            for j in range(cta):
+                f = oracle.canon_fields(o.get_state(j))
+                pc, mem = int(f["PC"]), f["mem"]
+                selfjump = pc < 0xFFF and (int(mem[pc]) << 8 | int(mem[pc + 1])) == (0x1000 | pc)
+                sl.append(bool(f["halted"]) or selfjump or (pc in loops and int(f["DT"]) > 0))
+            lane_frames += cta
+            sleeping += sum(sl)
+            warp_frames += cta // 32
+            skip_regroup += sum(sl) // 32
+            skip_ident += sum(all(sl[w * 32:(w + 1) * 32]) for w in range(cta // 32))
+            for j in range(cta):
+                o.run_cycles(j, ipf, keys[j])
+                o.tick_timers(j)
+    return {"sleeping_lane_frames": sleeping / lane_frames, "skippable_warp_frames_regrouped": skip_regroup / warp_frames,
+            "skippable_warp_frames_identity": skip_ident / warp_frames}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_workload_structure.md"))
@@ -189,6 +226,13 @@ def main():
                 rl.append(f"| {g} | {name} | {v['distinct_pcs']:.2f} | {v['distinct_classes']:.2f} | "
                           f"{100 * v['pc_uniform']:.1f}% | {100 * v['class_uniform']:.1f}% |")
                 print(rl[-1], flush=True)
+        rl += ["", "| game | env-frames slept through entirely | warp-frames skippable, identity grouping | "
+               "warp-frames skippable, regrouped by sleep status per frame |", "|---|---|---|---|"]
+        for g in args.games:
+            z = sleepers(g)
+            rl.append(f"| {g} | {100 * z['sleeping_lane_frames']:.1f}% | {100 * z['skippable_warp_frames_identity']:.1f}% | "
+                      f"{100 * z['skippable_warp_frames_regrouped']:.1f}% |")
+            print(rl[-1], flush=True)
         with open(args.regroup_out, "w") as f:
             f.write("# NEXT-2 regrouping study (oracle replay of one 128-env CTA, random actions)\n\n"
                     "Generated by `python -m tests.tools.workload_structure --regroup-out ...` "
