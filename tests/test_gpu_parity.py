@@ -786,8 +786,8 @@ def test_gymnax_env_matches_oracle():
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("startup", [None, [(1 << 1, 2)]])
-def test_pipelined_host_steps_match_device_steps(startup):
+@pytest.mark.parametrize("startup,obs_format", [(None, 0), ([(1 << 1, 2)], 0), (None, 1)])
+def test_pipelined_host_steps_match_device_steps(startup, obs_format):
     """octax_step_host / octax_step_host_frame at 262,144 envs step the envs in several chunk
     launches whose device->host copies overlap the next chunk's kernel: outputs equal a twin
     handle stepped with octax_step on the device, step by step, including synchronized
@@ -796,11 +796,12 @@ def test_pipelined_host_steps_match_device_steps(startup):
     over = dict(max_episode_steps=3)
     if startup:
         over["startup"] = startup
-    rom, spec = workloads.game("brix_standin", **over)
+    rom, spec = workloads.game("brix_standin", obs_format=obs_format, **over)
     n = 262144
     host_full, host_frame, dev = (OctaxEnv(rom, spec, n, 5) for _ in range(3))
     na = workloads.n_actions(spec)
-    o_h = np.zeros((n, 1024), np.uint8)
+    per = host_full.obs_per_env
+    o_h = np.zeros((n, per), np.uint8)
     f_h = np.zeros((n, 32, 8), np.uint8)
     r1, r2 = np.zeros(n, np.float32), np.zeros(n, np.float32)
     d1, d2 = np.zeros(n, np.uint8), np.zeros(n, np.uint8)
@@ -810,9 +811,13 @@ def test_pipelined_host_steps_match_device_steps(startup):
         host_full.step_host(a, o_h, r1, d1, t1)
         host_frame.step_host_frame(a, f_h, r2, d2, t2)
         obs, rew, done = dev.step(torch.from_numpy(a).cuda())
-        ob = obs.cpu().numpy().reshape(n, 1024)
+        ob = obs.cpu().numpy().reshape(n, per)
         assert np.array_equal(o_h, ob), t
-        assert np.array_equal(f_h.reshape(n, 256), ob[:, 768:]), t
+        if obs_format == 0:  # the frame is obs plane 3 in the packed layout
+            assert np.array_equal(f_h.reshape(n, 256), ob[:, 768:]), t
+        else:                # bool x-major plane 3 = the frame's pixels, transposed
+            bits = np.unpackbits(f_h.reshape(n, 32, 8), axis=2)          # [n][y][x]
+            assert np.array_equal(bits.transpose(0, 2, 1).reshape(n, 2048), ob[:, 3 * 2048:]), t
         rw, dn, tm = rew.cpu().numpy(), done.cpu().numpy(), dev.terminated.cpu().numpy()
         for r_, d_, t_ in ((r1, d1, t1), (r2, d2, t2)):
             assert np.array_equal(r_, rw) and np.array_equal(d_, dn) and np.array_equal(t_, tm), t
