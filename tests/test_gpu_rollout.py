@@ -230,10 +230,12 @@ def test_rollout_config4_sampled_parity_1000_steps(game):
     assert g.stats()[0][2] == n * R * T
 
 
-def test_rollout_without_obs_keeps_history():
+@pytest.mark.parametrize("obs_format", [0, 16])
+def test_rollout_without_obs_keeps_history(obs_format):
     """obs_out = NULL: rewards / dones (per-step strides) and states still match the oracle, and
-    the display history stays intact, so the obs of a step right after the rollout is exact."""
-    rom, spec = workloads.game("brix_standin", max_episode_steps=11)
+    the display history stays intact, so the obs of a step right after the rollout is exact
+    (default and stack-frames stacking)."""
+    rom, spec = workloads.game("brix_standin", max_episode_steps=11, obs_format=obs_format)
     n, T = 200, 13
     g = _env(rom, spec, n, 31)
     o = oracle.OracleEnv(rom, spec, n, 31)
