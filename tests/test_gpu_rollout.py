@@ -271,3 +271,34 @@ def test_rollout_generator_high_step_index_and_zero_length():
         assert np.array_equal(obs[k].cpu().numpy().reshape(n, -1), oo), k
         assert np.array_equal(rew[k].cpu().numpy(), orw) and np.array_equal(done[k].cpu().numpy(), od), k
     _check_states(g, o, list(range(n)))
+
+
+@pytest.mark.slow
+def test_default_horizon_truncation_10000_steps():
+    """The default max_episode_steps = 10,000 (A9) at scale: 4,096 Pong-spec envs (terminated "0",
+    so only truncation ends episodes) stepped 10,001 times in fused rollouts -- every env truncates
+    exactly once, at step 10,000, and sampled envs match the oracle in full state afterwards."""
+    rom, spec = workloads.game("pong_standin")
+    assert spec["max_episode_steps"] == 10000
+    n = 4096
+    g = _env(rom, spec, n, workloads.ENV_SEED)
+    _, rew, done, _, trunc = _outs(100, n)
+    dones = 0
+    for r in range(100):
+        g.rollout_into(100, None, rew, done, aseed=workloads.ACTION_SEED, t0=100 * r, truncated=trunc)
+        dones += int(done.sum().item())
+        if r < 99:
+            assert dones == 0
+    assert dones == n and bool(trunc[99].all())  # all at step 10,000 (the last of rollout 99)
+    _, rew1, done1, _, _ = _outs(1, n, per_step=False)
+    g.rollout_into(1, None, rew1, done1, aseed=workloads.ACTION_SEED, t0=10000)
+    s, _ = g.stats()
+    assert s[1] == n and s[2] == n * 10001
+    ids = [0, 1, 2047, n - 1]
+    st = g.get_states(ids)
+    na = workloads.n_actions(spec)
+    for k, gid in enumerate(ids):
+        o = oracle.OracleEnv(rom, spec, 1, workloads.ENV_SEED, gid)
+        for t in range(10001):
+            o.step(np.array([oracle.synthetic_action(workloads.ACTION_SEED, t, gid, na)], np.int32))
+        assert np.array_equal(st[k], o.get_state(0)), gid
