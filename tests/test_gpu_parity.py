@@ -857,3 +857,40 @@ def test_max_size_16M_envs_sampled_parity():
     s, _ = g.stats()
     assert s[2] == 3 * n and s[1] >= n  # every env truncated at step 2 (max_episode_steps = 2)
     g.close()
+
+
+def test_concurrent_handles_on_separate_streams():
+    """Handles are independent (include/octax.h): three games, each on its own CUDA stream,
+    launched interleaved without synchronisation between them (steps and fused rollouts), match
+    their oracles; a fourth handle on the default stream shares the device meanwhile."""
+    from paper_2510_01764_b200 import OctaxEnv
+    games = [("pong_standin", 300), ("brix_standin", 257), ("target_shooter_level1", 129)]
+    streams = [torch.cuda.Stream() for _ in games]
+    envs, oracles, specs = [], [], []
+    for (game, n), s in zip(games, streams):
+        rom, spec = workloads.game(game, max_episode_steps=9)
+        envs.append(OctaxEnv(rom, spec, n, 11, stream=s))
+        oracles.append(oracle.OracleEnv(rom, spec, n, 11))
+        specs.append(spec)
+    rom, spec = workloads.game("coverage")
+    bystander = OctaxEnv(rom, spec, 4096, 3)
+    acts = [[torch.from_numpy(workloads.gen.actions(7, t, n, workloads.n_actions(sp))).cuda()
+             for t in range(12)] for (g, n), sp in zip(games, specs)]
+    outs = [[] for _ in games]
+    torch.cuda.synchronize()
+    for t in range(12):
+        for k, (e, s) in enumerate(zip(envs, streams)):
+            with torch.cuda.stream(s):
+                e.step(acts[k][t])
+                outs[k].append((e.obs.clone(), e.reward.clone(), e.done.clone()))
+        bystander.step(torch.zeros(4096, dtype=torch.int32, device="cuda"))
+    torch.cuda.synchronize()
+    for k, ((game, n), o, sp) in enumerate(zip(games, oracles, specs)):
+        for t in range(12):
+            oo, orw, od, _, _ = o.step(workloads.gen.actions(7, t, n, workloads.n_actions(sp)))
+            go, gr, gd = outs[k][t]
+            assert np.array_equal(go.cpu().numpy().reshape(n, -1), oo), (game, t)
+            assert np.array_equal(gr.cpu().numpy(), orw) and np.array_equal(gd.cpu().numpy(), od), (game, t)
+        gs = envs[k].get_states(list(range(n)))
+        for j in range(n):
+            assert np.array_equal(gs[j], o.get_state(j)), (game, j)
