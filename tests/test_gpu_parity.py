@@ -861,7 +861,7 @@ def test_max_size_16M_envs_sampled_parity():
 
 def test_concurrent_handles_on_separate_streams():
     """Handles are independent (include/octax.h): three games, each on its own CUDA stream,
-    launched interleaved without synchronisation between them (steps and fused rollouts), match
+    launched interleaved without synchronisation between them, match
     their oracles; a fourth handle on the default stream shares the device meanwhile."""
     from paper_2510_01764_b200 import OctaxEnv
     games = [("pong_standin", 300), ("brix_standin", 257), ("target_shooter_level1", 129)]
