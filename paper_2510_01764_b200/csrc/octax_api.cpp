@@ -298,6 +298,15 @@ octax_status compile_expr(const char *src, const char *what, Program &prog) {
   for (size_t k = 0; k < c.out.size(); ++k) prog.ops[k] = c.out[k];
   prog.len = (uint32_t)c.out.size();
   prog.depth = (uint32_t)c.max_depth;
+  const ExprInsn *o = prog.ops;
+  if (prog.len == 1 && o[0].op == X_CONST) {
+    prog.kind = 1; prog.ka = o[0].imm;                      // "0"
+  } else if (prog.len == 1 && o[0].op == X_V) {
+    prog.kind = 2; prog.ka = o[0].arg;                      // "V5"
+  } else if (prog.len == 3 && o[0].op == X_V && o[1].op == X_CONST && (o[2].op == X_EQ || o[2].op == X_NE)) {
+    prog.kind = o[2].op == X_EQ ? 3u : 4u;                  // "V14 == 0", "V3 != 1"
+    prog.ka = o[0].arg; prog.kb = o[1].imm;
+  }
   return OCTAX_OK;
 }
 

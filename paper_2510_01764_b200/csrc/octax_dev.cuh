@@ -125,6 +125,10 @@ struct Program {
   ExprInsn ops[kMaxOps];
   uint32_t len;
   uint32_t depth;
+  // the program's shape when it is one of the common one- to three-op forms, evaluated without
+  // the bytecode loop: 0 = general, 1 = constant ka, 2 = V[ka], 3 = V[ka] == kb, 4 = V[ka] != kb
+  uint32_t kind;
+  uint32_t ka, kb;
 };
 
 // Device-resident per-env state, structure-of-arrays (one entry per local env).
