@@ -640,13 +640,12 @@ __device__ __forceinline__ void run_frames(Smem &sm, Lane &L, const StepParams &
 // program).  The stack lives in registers as a shift register with compile-time
 // slots (depth <= kMaxDepth is enforced at create), so it costs no shared memory.
 __device__ __forceinline__ uint32_t eval(const Program &P, Smem &sm, const StepParams &p, const Lane &L, int tid) {
-#ifdef OCTAX_EVAL_FAST
-  // the common shapes (uniform branches on the compiled program's kind): no bytecode loop
+  // the common shapes (uniform branches on the compiled program's kind, set at create): no
+  // bytecode loop (A/B: +0.2% pong, +0.6..1.0% brix / Target Shooter, whose specs are all of them)
   if (P.kind == 1u) return P.ka;
   if (P.kind == 2u) return (uint32_t)VREG(P.ka);
   if (P.kind == 3u) return (uint32_t)VREG(P.ka) == P.kb ? 1u : 0u;
   if (P.kind == 4u) return (uint32_t)VREG(P.ka) != P.kb ? 1u : 0u;
-#endif
   uint32_t st[kMaxDepth];
 #pragma unroll
   for (int k = 0; k < kMaxDepth; ++k) st[k] = 0;
