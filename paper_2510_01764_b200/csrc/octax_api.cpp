@@ -290,6 +290,32 @@ octax_status compile_expr(const char *src, const char *what, Program &prog) {
     if (!c.bad && c.toks[c.i].k != T_END) c.fail(c.toks[c.i].at, "unexpected trailing input");
   }
   if (c.bad) return set_err(OCTAX_E_EXPR, "%s: %s at byte %zu", what, c.msg.c_str(), c.bad_at);
+  // peephole: "V[n] c /" and "V[n] c %" become one push of V[n] / c (% c) by multiply-shift;
+  // the byte V[n] < 256 makes q = (V * (2^16 / c + 1)) >> 16 exact for every c <= 255 (error
+  // < V / 2^16 < 1 / c); c > 255 gives q = 0; c = 0 keeps x / 0 = x % 0 = 0 (A28)
+  {
+    std::vector<ExprInsn> o;
+    for (size_t k = 0; k < c.out.size(); ++k) {
+      if (k + 2 < c.out.size() && c.out[k].op == X_V && c.out[k + 1].op == X_CONST &&
+          (c.out[k + 2].op == X_DIV || c.out[k + 2].op == X_MOD)) {
+        const uint32_t d = c.out[k + 1].imm;
+        ExprInsn f{};
+        if (d == 0) {
+          f.op = X_CONST;
+        } else {
+          f.op = c.out[k + 2].op == X_DIV ? X_VDIV : X_VMOD;
+          f.arg = c.out[k].arg;
+          f.pad = (uint16_t)(d > 255u ? 256u : d);  // only used when d <= 255 (q = 0 above)
+          f.imm = d > 255u ? 0u : 65536u / d + 1u;
+        }
+        o.push_back(f);
+        k += 2;
+        continue;
+      }
+      o.push_back(c.out[k]);
+    }
+    c.out.swap(o);
+  }
   if (c.out.size() > (size_t)kMaxOps)
     return set_err(OCTAX_E_EXPR, "%s: expression longer than %u ops", what, (unsigned)kMaxOps);
   if (c.max_depth > kMaxDepth)

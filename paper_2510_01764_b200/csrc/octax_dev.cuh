@@ -109,7 +109,11 @@ inline void make_entry(uint32_t op, const uint32_t *dtab, uint32_t quirks, uint3
 
 // expression bytecode (postfix, evaluated with top-of-stack in a register)
 enum ExprOp : uint8_t {
-  X_CONST = 0, X_V, X_I, X_DT, X_ST, X_MEM, X_NEG, X_NOT, X_BNOT,
+  X_CONST = 0, X_V, X_I, X_DT, X_ST,
+  X_VDIV, X_VMOD,  // push V[arg] / c, V[arg] % c for a constant c = pad (fused at create from
+                   // "V[n] c /" and "V[n] c %"): q = (V * imm) >> 16, imm = 2^16 / c + 1, exact for
+                   // the byte V when c <= 255; imm = 0 for c > 255 (q = 0)
+  X_MEM, X_NEG, X_NOT, X_BNOT,
   X_MUL, X_DIV, X_MOD, X_ADD, X_SUB, X_SHL, X_SHR,
   X_LT, X_LE, X_GT, X_GE, X_EQ, X_NE, X_AND, X_XOR, X_OR, X_LAND, X_LOR
 };

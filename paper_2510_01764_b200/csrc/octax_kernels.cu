@@ -651,11 +651,15 @@ __device__ __forceinline__ uint32_t eval(const Program &P, Smem &sm, const StepP
   for (int k = 0; k < kMaxDepth; ++k) st[k] = 0;
   for (uint32_t i = 0; i < P.len; ++i) {
     const ExprInsn in = P.ops[i];
-    if (in.op <= X_ST) {  // push
-      const uint32_t v = in.op == X_CONST ? in.imm
-                       : in.op == X_V   ? (uint32_t)VREG(in.arg)
-                       : in.op == X_I   ? (L.I & 0xFFFFu)
-                       : in.op == X_DT  ? L.dt : L.st;
+    if (in.op <= X_VMOD) {  // push
+      uint32_t v = in.op == X_CONST ? in.imm
+                 : in.op <= X_V || in.op >= X_VDIV ? (uint32_t)VREG(in.arg)
+                 : in.op == X_I   ? (L.I & 0xFFFFu)
+                 : in.op == X_DT  ? L.dt : L.st;
+      if (in.op >= X_VDIV) {  // byte / constant by multiply-shift (X_VDIV), remainder (X_VMOD)
+        const uint32_t q = (v * in.imm) >> 16;
+        v = in.op == X_VDIV ? q : v - q * (uint32_t)in.pad;
+      }
 #pragma unroll
       for (int k = kMaxDepth - 1; k > 0; --k) st[k] = st[k - 1];
       st[0] = v;

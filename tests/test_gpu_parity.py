@@ -233,7 +233,8 @@ def test_random_state_fuzz_parity(quirks):
 EXPRS = ["V5", "(V14 // 10) - (V14 % 10)", "(V9 == 0) | (V12 >= 0x3E)", "V1 == 2",
          "mem[I] + mem[I + 1] * 256", "-V3 ^ ~V4", "V1 << V2 | V3 >> V4", "V1 / V2 + V3 % V4",
          "!(V1 && V2) || V3 < V4 && V5 >= V6", "DT * ST - I", "mem[V0 * 16 + V1]",
-         "((V1 + 2) * (V2 + 3) - (V3 + 4) * (V4 + 5)) / (V6 - V7 + 1)"]
+         "((V1 + 2) * (V2 + 3) - (V3 + 4) * (V4 + 5)) / (V6 - V7 + 1)",
+         "V3 // 7 - V4 % 0 + (V5 % 300) * 2 + V14 // 1 - mem[V2 // 16]"]  # fused V // c, V % c pushes
 
 
 @pytest.mark.parametrize("expr", EXPRS)
@@ -894,3 +895,25 @@ def test_concurrent_handles_on_separate_streams():
         gs = envs[k].get_states(list(range(n)))
         for j in range(n):
             assert np.array_equal(gs[j], o.get_state(j)), (game, j)
+
+
+@pytest.mark.parametrize("c", [0, 1, 2, 3, 5, 7, 10, 13, 100, 127, 128, 200, 255, 256, 1000])
+def test_expression_register_by_constant_division_exhaustive(c):
+    """`V[n] // c` and `V[n] % c` are fused at create into one multiply-shift push (exact for the
+    byte V and c <= 255; c > 255 gives 0 / V; c = 0 gives 0, A28): every byte value of V0 in its own
+    env, the score `(V0 // c) + (V0 % c) * 1000 + (V1 % c)` vs the oracle's parser."""
+    expr = f"(V0 // {c}) + (V0 % {c}) * 1000 + (V1 % {c})"
+    rom = bytes([0x12, 0x00])
+    n = 256
+    spec = dict(workloads.DEFAULTS, score=expr, terminated="0", action_keys=[1],
+                frame_skip=1, instructions_per_frame=1, max_episode_steps=0)
+    g = _gpu_env(rom, spec, n, 1)
+    base = oracle.canon_fields(g.get_state(0))
+    for j in range(n):
+        g.set_state(j, canon(V=[j, 255 - j] + [0] * 14, PC=0x200, mem=base["mem"], display=base["display"],
+                             hist=base["hist"]))
+    g.step(torch.zeros(n, dtype=torch.int32, device="cuda"))
+    st = g.get_states(list(range(n)))
+    for j in range(n):
+        want = oracle.eval_expr(expr, st[j])
+        assert oracle.canon_fields(st[j])["prev_score"] == want, (c, j)
