@@ -209,10 +209,11 @@ octax_status octax_gen_actions(octax_env *e, uint64_t aseed, uint64_t t, int32_t
  *  - obs_out may be NULL: no observation is written (rewards / dones only, e.g. policy-free
  *    evaluation); the display history is still kept, so later steps' obs are unaffected.
  *  - a non-zero stride must cover all n envs (obs: >= n * 1024 bytes; outputs: >= n).
- * Same-step auto-reset (A10) runs inline, also for specs with startup segments.  Packed obs
- * only: a handle created with OCTAX_OBS_BOOL_XMAJOR gets OCTAX_E_INVALID_ARG (either stacking
- * mode is supported).  T = 0 is a no-op.  Stream-ordered, no host synchronisation; the
- * statistics count all T steps. */
+ * Same-step auto-reset (A10) runs inline, also for specs with startup segments.  Either
+ * stacking mode; either layout: with OCTAX_OBS_BOOL_XMAJOR the kernel writes packed obs to a
+ * library staging buffer ([T][n] packed, or the last step's with stride 0) that
+ * expand_obs_kernel expands into obs_out after it (obs_step_stride 0 or n * 8192).  T = 0 is a
+ * no-op.  Stream-ordered, no host synchronisation; the statistics count all T steps. */
 octax_status octax_rollout(octax_env *e, uint32_t T, const int32_t *actions, uint64_t aseed, uint64_t t0,
                            void *obs_out, uint64_t obs_step_stride, float *reward_out, uint8_t *done_out,
                            uint8_t *terminated_out, uint8_t *truncated_out, uint64_t out_step_stride);

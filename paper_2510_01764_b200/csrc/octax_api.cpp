@@ -395,6 +395,8 @@ struct octax_env {
   size_t block_bytes = 0;
   uint8_t *packed_scratch = nullptr;  // packed obs staging for the bool format
   uint8_t *final_scratch = nullptr;   // packed final-obs staging for the bool format (lazy)
+  uint8_t *roll_scratch = nullptr;    // packed [T][n] obs staging of bool-format rollouts (lazy)
+  uint64_t roll_scratch_bytes = 0;
   // host-step staging (lazy)
   int32_t *d_actions = nullptr;
   uint8_t *d_obs = nullptr;
@@ -417,6 +419,7 @@ static void free_env(octax_env *e) {
   cudaFree(e->block);
   cudaFree(e->packed_scratch);
   cudaFree(e->final_scratch);
+  cudaFree(e->roll_scratch);
   cudaFree(e->d_actions);
   cudaFree(e->d_obs);
   cudaFree(e->d_reward);
@@ -701,8 +704,6 @@ extern "C" octax_status octax_rollout(octax_env *e, uint32_t T, const int32_t *a
   if (!e || !reward_out || !done_out)
     return set_err(OCTAX_E_INVALID_ARG, "NULL argument to octax_rollout");
   if (T == 0) return OCTAX_OK;
-  if (e->obs_format != OCTAX_OBS_PACKED)
-    return set_err(OCTAX_E_INVALID_ARG, "octax_rollout: packed observations only (obs_format OCTAX_OBS_PACKED)");
   if (obs_step_stride % 16 != 0)
     return set_err(OCTAX_E_INVALID_ARG, "octax_rollout: obs_step_stride must be a multiple of 16 bytes");
   if (!obs_out) obs_step_stride = 0;
@@ -720,11 +721,35 @@ extern "C" octax_status octax_rollout(octax_env *e, uint32_t T, const int32_t *a
   p.T = T;
   p.aseed = aseed;
   p.t0 = t0;
-  p.obs_stride = obs_step_stride / 8;
   p.out_stride = out_step_stride;
-  CU(launch_step(p, MODE_ROLLOUT, actions, (uint8_t *)obs_out, reward_out, done_out, terminated_out, truncated_out,
-                 e->stream),
+  uint8_t *packed = (uint8_t *)obs_out;
+  uint64_t planes_out = 0;  // bool layout: packed obs planes to expand after the kernel
+  if (obs_out && e->obs_format != OCTAX_OBS_PACKED) {
+    // the bool [n,4,64,32] layout: the kernel writes packed obs, expand_obs_kernel expands them
+    // after it -- every step's (a [T][n] packed staging buffer) or, with stride 0, the last step's
+    if (obs_step_stride == 0) {
+      packed = e->packed_scratch;
+      planes_out = e->n;
+    } else {
+      if (obs_step_stride != (uint64_t)e->obs_bytes * e->n)
+        return set_err(OCTAX_E_INVALID_ARG, "octax_rollout: bool observations need stride 0 or n * 8192 bytes");
+      const uint64_t need = (uint64_t)T * e->n * 1024;
+      if (need > e->roll_scratch_bytes) {
+        cudaFree(e->roll_scratch);
+        e->roll_scratch = nullptr;
+        e->roll_scratch_bytes = 0;
+        CU(cudaMalloc(&e->roll_scratch, need), "cudaMalloc(rollout obs staging)");
+        e->roll_scratch_bytes = need;
+      }
+      packed = e->roll_scratch;
+      planes_out = (uint64_t)T * e->n;
+      obs_step_stride = 1024 * e->n;
+    }
+  }
+  p.obs_stride = obs_step_stride / 8;
+  CU(launch_step(p, MODE_ROLLOUT, actions, packed, reward_out, done_out, terminated_out, truncated_out, e->stream),
      "rollout kernel");
+  if (planes_out) CU(launch_expand_obs(planes_out, packed, (uint8_t *)obs_out, e->stream), "expand obs");
   e->p.head = (e->p.head + T) & 3u;
   return OCTAX_OK;
 }

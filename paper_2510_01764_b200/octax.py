@@ -227,17 +227,17 @@ class OctaxEnv:
     def rollout_into(self, T: int, obs, reward, done, actions=None, aseed: int = 0, t0: int = 0,
                      terminated=None, truncated=None):
         """Fused rollout (octax_rollout): T steps in one launch.  actions: int32 [T, n] or None
-        (in-kernel generator for steps t0..t0+T-1 under aseed).  obs: uint8 [T, n, 4, 32, 8]
-        (every step kept), [n, 4, 32, 8] (overwritten; the last step remains) or None (no
+        (in-kernel generator for steps t0..t0+T-1 under aseed).  obs: uint8 [T, n, *obs shape]
+        (every step kept), [n, *obs shape] (overwritten; the last step remains) or None (no
         observations written); reward / done /
         terminated / truncated: [T, n] or [n], likewise."""
         import torch
         n, T = self.n, int(T)
         if T == 0:  # octax_rollout's no-op
             return
-        ob = 1024 * n
+        ob = self.obs_per_env * n
         if obs is not None and obs.numel() not in (ob, T * ob):
-            raise ValueError(f"obs must hold n or T*n packed observations, got {obs.numel()} bytes")
+            raise ValueError(f"obs must hold n or T*n observations, got {obs.numel()} bytes")
         obs_stride = ob if obs is not None and obs.numel() == T * ob and T > 1 else 0
         outs = [reward, done, terminated, truncated]
         sizes = {t.numel() for t in outs if t is not None}

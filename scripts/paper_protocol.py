@@ -196,7 +196,7 @@ def main():
     from bench import ClockSampler
     jobs = []
     for cid, game, n, fmt, mode, warm in [c + (0,) for c in CONFIGS] + [c + (1000,) for c in MIXED]:
-        launches = ["step", "fused"] if fmt == 0 else ["step"]  # octax_rollout: packed obs only
+        launches = ["step", "fused"]
         if n <= 65536 and not warm:
             launches.append("graph")
         jobs += [(cid, game, n, fmt, mode, warm, ln) for ln in launches]

@@ -153,14 +153,8 @@ def test_rollout_equals_steps_on_gpu_at_4096():
 
 
 def test_rollout_rejects_bad_arguments():
-    from paper_2510_01764_b200.octax import OctaxError
-    rom, spec = workloads.game("pong_standin", obs_format=1)
-    g = _env(rom, spec, 64, 1)
-    obs = torch.zeros((64, 4, 64, 32), dtype=torch.uint8, device="cuda")
     r = torch.zeros(64, dtype=torch.float32, device="cuda")
     d = torch.zeros(64, dtype=torch.uint8, device="cuda")
-    with pytest.raises((OctaxError, ValueError)):
-        g.rollout_into(4, obs, r, d)  # bool obs handle: packed only
     rom, spec = workloads.game("pong_standin")
     g = _env(rom, spec, 64, 1)
     obs = torch.zeros((64, 4, 32, 8), dtype=torch.uint8, device="cuda")
@@ -302,3 +296,30 @@ def test_default_horizon_truncation_10000_steps():
         for t in range(10001):
             o.step(np.array([oracle.synthetic_action(workloads.ACTION_SEED, t, gid, na)], np.int32))
         assert np.array_equal(st[k], o.get_state(0)), gid
+
+
+@pytest.mark.parametrize("per_step", [True, False])
+def test_rollout_bool_obs_parity(per_step):
+    """OCTAX_OBS_BOOL_XMAJOR handles (the paper's (4, 64, 32) boolean obs): the rollout
+    kernel writes packed obs into a library staging buffer and expand_obs_kernel expands them --
+    every step's with per-step strides, the last step's with stride 0 -- equal to the oracle's."""
+    rom, spec = workloads.game("brix_standin", obs_format=1, max_episode_steps=7)
+    n, T = 150, 9
+    g = _env(rom, spec, n, 4)
+    o = oracle.OracleEnv(rom, spec, n, 4)
+    na = workloads.n_actions(spec)
+    acts = np.stack([workloads.gen.actions(6, k, n, na) for k in range(T)])
+    shape = ((T,) if per_step else ()) + (n, 4, 64, 32)
+    obs = torch.zeros(shape, dtype=torch.uint8, device="cuda")
+    rew = torch.zeros(((T,) if per_step else ()) + (n,), dtype=torch.float32, device="cuda")
+    done = torch.zeros(((T,) if per_step else ()) + (n,), dtype=torch.uint8, device="cuda")
+    g.rollout_into(T, obs, rew, done, actions=torch.from_numpy(acts).cuda())
+    for k in range(T):
+        oo, orw, od, _, _ = o.step(acts[k])
+        if per_step:
+            assert np.array_equal(obs[k].cpu().numpy().reshape(n, -1), oo), k
+            assert np.array_equal(rew[k].cpu().numpy(), orw) and np.array_equal(done[k].cpu().numpy(), od), k
+    if not per_step:
+        assert np.array_equal(obs.cpu().numpy().reshape(n, -1), oo)
+        assert np.array_equal(rew.cpu().numpy(), orw) and np.array_equal(done.cpu().numpy(), od)
+    _check_states(g, o, list(range(n)))
