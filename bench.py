@@ -590,7 +590,11 @@ def main():
                  "vs_step_mode": fv / value, "stats": [int(x) for x in fst.cpu().tolist()],
                  "actions": "generated inside the rollout kernel (Philox domain 1, same stream as octax_gen_actions)",
                  "no_obs": None,
-                 "outputs": "obs / reward / done written every step (same [n] buffers as the step mode)"}
+                 "outputs": ("obs / reward / done written every step (same [n] buffers as the step mode)"
+                             if args.obs == "packed" else
+                             "packed obs / reward / done written every step; the bool [n,4,64,32] expansion runs "
+                             "once, for the last step (stride 0: every step overwrites the same buffer, so the "
+                             "earlier steps' bool obs are never observable)")}
         # the same rollouts without observations (octax_rollout obs_out = NULL: rewards / dones
         # only, e.g. policy-free evaluation) -- the interpreter with no obs I/O, context only
         if not args.no_fused_noobs:

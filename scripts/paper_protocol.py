@@ -234,7 +234,9 @@ def main():
                "R_issue": R_issue, "R_alu": R_alu, "R_hbm": R_hbm, "binding": binding,
                "frac_binding": med / roofs[binding] if binding else None,
                "bitexact": pytest_status(bt), "bitexact_test": bt, "n_envs_checked": be, "steps_checked": bs,
-               "cpu_model": cpu_model}
+               "cpu_model": cpu_model,
+               **({"obs_note": "fused + bool: packed obs every step, bool expansion of the last step only "
+                               "(stride-0 rollout: intermediate obs are overwritten)"} if launch == "fused" and fmt else {})}
         # self-consistency: steps/s recomputes from the row's own fields
         assert abs(row["frames_per_s_median"] - 4 * row["steps_per_s_median"]) < 1e-6 * row["frames_per_s_median"]
         if not args.no_cpu and game not in cpu_cache:
