@@ -256,7 +256,8 @@ def main():
              "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         roof = f"{r['binding']} ({r['frac_binding']:.2f})" if r["binding"] else "-"
-        lines.append(f"| {r['config']} | {r['game']} | {r['envs']:,} | {r['obs']} | {r['mode']} | {r['actions']} | "
+        mode = r["mode"] + (" (bool expanded for the last step)" if r.get("obs_note") else "")
+        lines.append(f"| {r['config']} | {r['game']} | {r['envs']:,} | {r['obs']} | {mode} | {r['actions']} | "
                      f"{r['protocol']} | {r['steps_per_s_median']:.4g} | {r['steps_per_s_iqr']:.3g} | "
                      f"{r['frames_per_s_median']:.4g} | {r['sm_clock_mhz_during']} | {roof} | "
                      f"{r['bitexact']} ({r['n_envs_checked']} x {r['steps_checked']}) | "

@@ -30,7 +30,7 @@ def table(tag):
         st, gr, fu = m["step"], m.get("graph"), m.get("fused")
         out.append(f"| {k[0]} | {k[1]} | {k[2]:,} | {k[3]} | {k[4]} | {k[5]} | {f(st['steps_per_s_median'])} "
                    f"({f(st['steps_per_s_iqr'])}) | {f(gr['steps_per_s_median']) if gr else '—'} | "
-                   f"{f(fu['steps_per_s_median']) if fu else '—'} | {b(st)} | {b(fu)} | "
+                   f"{f(fu['steps_per_s_median']) + (' †' if fu.get('obs_note') else '') if fu else '—'} | {b(st)} | {b(fu)} | "
                    f"{f(st.get('oracle_1core', float('nan')))} | {f(st.get('oracle_all_cores', float('nan')))} |")
     return "\n".join(out) + "\n"
 
