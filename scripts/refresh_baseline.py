@@ -59,7 +59,7 @@ def main():
     p = os.path.join(ROOT, "BASELINE.md")
     s = open(p).read()
     a = s.index("| Config | Game / ROM | n per GPU | Obs | Actions | Protocol | step: steps/s (IQR)")
-    b = s.index("\nBool obs at 1M envs")
+    b = s.index("\n† A fused rollout") if "\n† A fused rollout" in s else s.index("\nBool obs at 1M envs")
     s = s[:a] + table(tag) + s[b:]
     a = s.index("Headline (`bench.py`, `profiles/")
     b = s.index("The fused mode beats launch-by-launch")
