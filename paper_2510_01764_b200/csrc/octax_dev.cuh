@@ -91,11 +91,6 @@ inline void make_entry(uint32_t op, const uint32_t *dtab, uint32_t quirks, uint3
   if (op == 0x00EEu) f |= E_RET;
   if (op == 0x00E0u) f |= E_CLS;
   if ((f & (E_CLS | D_RND | D_MEM)) != 0u) f |= D_RARE;
-#ifdef OCTAX_PRMT_VX
-  // bits 28..30: where a VX write takes its value, as a byte selector over
-  // {nn, VX + nn, ALU result, DT, lowest held key} (E_VSRC)
-  f |= ((f & D_WAIT) ? 4u : (f & D_VSDT) ? 3u : (f & D_VSALU) ? 2u : (f & D_VSADD) ? 1u : 0u) << 28;
-#endif
   const uint32_t dsp = (f & E_RET) ? 0u : (f & D_CALL) ? 2u : 1u;
   const uint32_t rx = ((d & D_BJMP) != 0u && (quirks & 4u) == 0u) ? 0u : x;  // 4 = OCTAX_Q_JUMP_VX
   ex = f;

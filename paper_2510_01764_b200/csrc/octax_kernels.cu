@@ -535,17 +535,11 @@ __device__ __forceinline__ void cycle(Smem &sm, Lane &L, const StepParams &p, in
   const uint32_t r8 = s8;  // stored as a byte: no masking
   // ---- register writes
 
-#ifdef OCTAX_PRMT_VX
-  // the VX value as one byte permute over the five candidate bytes, selected by the entry
-  const uint32_t cand = __byte_perm(__byte_perm(nn, vx + nn, 0x0040), __byte_perm(r8, L.dt, 0x0040), 0x5410);
-  const uint32_t nvx = __byte_perm(cand, L.kidx, d >> 28);
-#else
   uint32_t nvx = nn;
   nvx = HAS(d, D_VSADD) ? (vx + nn) : nvx;
   nvx = HAS(d, D_VSALU) ? r8 : nvx;
   nvx = HAS(d, D_VSDT) ? L.dt : nvx;
   nvx = HAS(d, D_WAIT) ? L.kidx : nvx;
-#endif
   sm.V[ax] = (uint8_t)((ex && (d & L.wvm) != 0u) ? nvx : vx);  // unconditional: no branch around the ALU
   if (ex && HAS(d, D_WVF)) VREG(15) = (uint8_t)f8;
   // ---- control flow and index / timer registers
