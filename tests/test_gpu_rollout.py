@@ -323,3 +323,13 @@ def test_rollout_bool_obs_parity(per_step):
         assert np.array_equal(obs.cpu().numpy().reshape(n, -1), oo)
         assert np.array_equal(rew.cpu().numpy(), orw) and np.array_equal(done.cpu().numpy(), od)
     _check_states(g, o, list(range(n)))
+
+
+@pytest.mark.parametrize("fseed", list(range(6)))
+def test_rollout_fuzz_rom_parity(fseed):
+    """The fuzz ROMs of test_gpu_parity (weighted mix of all 35 forms, self-modifying stores,
+    faults, CXNN) through fused rollouts of uneven lengths, every step against the oracle."""
+    rom = workloads.gen.fuzz_rom(fseed, n_instr=200 + 40 * fseed)
+    spec = dict(workloads.DEFAULTS, score="V0 + (V1 << 8) + mem[0x300]", terminated="0",
+                action_keys=list(range(16)), max_episode_steps=40 + 13 * fseed)
+    _rollout_vs_oracle(rom, spec, 160, [11, 50, 1, 30], 1000 + fseed, fseed)
