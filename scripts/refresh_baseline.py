@@ -62,7 +62,7 @@ def main():
     b = s.index("\n† A fused rollout") if "\n† A fused rollout" in s else s.index("\nBool obs at 1M envs")
     s = s[:a] + table(tag) + s[b:]
     a = s.index("Headline (`bench.py`, `profiles/")
-    b = s.index("The fused mode beats launch-by-launch")
+    b = s.index("At the paper's own scale") if "At the paper's own scale" in s else s.index("The fused mode beats launch-by-launch")
     s = s[:a] + headline(tag) + s[b:]
     s = re.sub(r"kernel v\d+ \(`profiles/r02_v\d+_paper_protocol\.\{json,md\}`;",
                f"kernel {tag.split('_')[1]} (`profiles/{tag}_paper_protocol.{{json,md}}`;", s)
