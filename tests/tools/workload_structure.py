@@ -210,13 +210,129 @@ def sleepers(game, warm=300, steps=24, cta=128):
             "skippable_warp_frames_identity": skip_ident / warp_frames}
 
 
+def draw_traces(game, warm=300, steps=24, cta=128):
+    """Per frame, per env, per instruction slot k < ipf: the rows the instruction at slot k draws
+    (0 = not a DXYN).  An env's instruction stream does not depend on how its warp schedules
+    it, so every scheduling policy below replays these same traces."""
+    rom, spec = workloads.game(game)
+    ipf, fs = spec["instructions_per_frame"], spec["frame_skip"]
+    o = oracle.OracleEnv(rom, spec, cta, workloads.ENV_SEED)
+    na = workloads.n_actions(spec)
+    for t in range(warm):
+        o.step(workloads.gen.actions(workloads.ACTION_SEED, t, cta, na))
+    frames = []
+    for t in range(warm, warm + steps):
+        a = workloads.gen.actions(workloads.ACTION_SEED, t, cta, na)
+        keys = [0 if x == 0 else 1 << spec["action_keys"][x - 1] for x in a]
+        for _ in range(fs):
+            fr = np.zeros((cta, ipf), np.int32)
+            for j in range(cta):
+                for k in range(ipf):
+                    f = oracle.canon_fields(o.get_state(j))
+                    pc, mem = int(f["PC"]), f["mem"]
+                    word = (int(mem[pc]) << 8 | int(mem[pc + 1])) if pc < 0xFFF else 0
+                    if word >> 12 == 0xD and not f["halted"]:  # clipped rows (A18), >= 1 marks a draw
+                        fr[j, k] = max(1, min(word & 15, 32 - (int(f["V"][(word >> 4) & 15]) & 31)))
+                    o.run_cycles(j, 1, keys[j])
+                o.tick_timers(j)
+            frames.append(fr)
+    return frames
+
+
+# warp instructions per warp-cycle, from profiles/r02_v42_source_attr_1M.md (pong, 1M envs):
+# the interpreter core without the draw paths ~118 (rounded to 120; 80 as a what-if for a much
+# cheaper core), and per DXYN dispatch, by the kernel's path choice: grouped ~65, single-row ~24,
+# lane-parallel ~15 + 14 per row step, cooperative ~200, each + ~10 for the votes / reduce
+def _draw_cost(rows):
+    k, mx = len(rows), max(rows)
+    if mx >= 3 and k * mx <= 32:
+        return 10 + 65
+    if mx == 1:
+        return 10 + 25
+    return 10 + (15 + 14 * mx if mx <= 8 else 200)
+
+
+def _batched_frame(fr, core, K=None, W=None):
+    """One warp's frame (fr: [32, ipf]) under draw batching: a lane reaching a DXYN waits (no
+    effect, PC held) until the warp fires a batch -- when K lanes wait, a lane has waited W
+    iterations, or no other unfinished lane can advance; K=None is the kernel as built (every
+    DXYN drawn in the cycle it is reached).  The warp iterates until every lane has executed
+    its ipf instructions.  Returns (iterations, draw dispatches, cost in warp instructions)."""
+    n, ipf = fr.shape
+    cnt, wait = np.zeros(n, np.int64), np.zeros(n, np.int64)
+    it = dr = 0
+    cost = 0.0
+    while (cnt < ipf).any():
+        it += 1
+        cost += core
+        live = np.nonzero(cnt < ipf)[0]
+        rows = fr[live, cnt[live]]
+        cnt[live[rows == 0]] += 1
+        pend = live[rows != 0]
+        if pend.size == 0:
+            continue
+        others = live.size - pend.size
+        if K is None or pend.size >= K or others == 0 or wait[pend].max() + 1 >= W:
+            cost += _draw_cost(fr[pend, cnt[pend]].tolist())
+            dr += 1
+            cnt[pend] += 1
+            wait[pend] = 0
+        else:
+            wait[pend] += 1
+    return it, dr, cost
+
+
+BATCH_POLICIES = [(None, None), (4, 3), (8, 4), (8, 8), (16, 6), (32, 10 ** 9)]
+
+
+def draw_batching(game, core=120.0, frames=None):
+    """NEXT-2 / P:289 "adaptive batching", read as batching the DXYN draws of a warp: lanes that
+    reach a draw wait so that one draw dispatch serves several of them.  Cost of each policy
+    relative to the kernel as built, over the 4 warps of one 128-env CTA."""
+    frames = draw_traces(game) if frames is None else frames
+    out = {}
+    for pol in BATCH_POLICIES:
+        tot = np.zeros(3)
+        for fr in frames:
+            for w in range(fr.shape[0] // 32):
+                tot += _batched_frame(fr[32 * w: 32 * w + 32], core, *pol)
+        out[pol] = tot
+    base = out[(None, None)][2]
+    return {pol: {"iterations": int(v[0]), "draws": int(v[1]), "rel_cost": v[2] / base} for pol, v in out.items()}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_workload_structure.md"))
     ap.add_argument("--games", nargs="*", default=GAMES)
     ap.add_argument("--regroup-out", default=None,
                     help="also write the NEXT-2 regrouping study (regroup()) to this file")
+    ap.add_argument("--batching-out", default=None,
+                    help="write the NEXT-2 draw-batching study (draw_batching()) to this file")
     args = ap.parse_args()
+    if args.batching_out:
+        bl = ["| game | policy (fire at K waiting / W iterations) | warp iterations | draw dispatches | "
+              "cost, core 120 | cost, core 80 |", "|---|---|---|---|---|---|"]
+        for g in args.games:
+            tr = draw_traces(g)
+            r120, r80 = draw_batching(g, 120.0, tr), draw_batching(g, 80.0, tr)
+            for pol in BATCH_POLICIES:
+                name = "as built (draw when reached)" if pol[0] is None else \
+                    ("K=32 (all wait)" if pol[1] > 10 ** 6 else f"K={pol[0]}, W={pol[1]}")
+                v = r120[pol]
+                bl.append(f"| {g} | {name} | {v['iterations']} | {v['draws']} | {v['rel_cost']:.3f} | "
+                          f"{r80[pol]['rel_cost']:.3f} |")
+                print(bl[-1], flush=True)
+        with open(args.batching_out, "w") as f:
+            f.write("# NEXT-2 draw-batching study (oracle traces of one 128-env CTA, random actions)\n\n"
+                    "Generated by `python -m tests.tools.workload_structure --batching-out ...` "
+                    "(`draw_batching()`): 24 steps after a 300-step warm-up.  A lane that reaches a "
+                    "DXYN waits until its warp fires a batched draw; the warp iterates until every lane "
+                    "has run its ipf instructions.  Cost = warp iterations x core + draw dispatches x "
+                    "path cost (warp instructions, model constants in the tool, from "
+                    "`profiles/r02_v42_source_attr_1M.md`), relative to the kernel as built; the gating "
+                    "of waiting lanes is not even charged.\n\n" + "\n".join(bl) + "\n")
+        return
     if args.regroup_out:
         rl = ["| game | grouping | distinct PCs / warp-cycle | distinct classes / warp-cycle | "
               "PC-uniform warp-cycles | class-uniform warp-cycles |", "|---|---|---|---|---|---|"]
