@@ -68,8 +68,8 @@ def main():
                f"kernel {tag.split('_')[1]} (`profiles/{tag}_paper_protocol.{{json,md}}`;", s)
     s = re.sub(r"\(`profiles/r02_v\d+_full_\*`;", f"(`profiles/{tag}_full_*`;", s)
     n_pass = re.search(r"(\d+) passed", open(os.path.join(ROOT, "profiles", f"{tag}_pytest_gpu.log")).read())
-    s = re.sub(r"same box \(`profiles/r02_v\d+_pytest_gpu\.log`: \d+ passed;",
-               f"same box (`profiles/{tag}_pytest_gpu.log`: {n_pass.group(1) if n_pass else '?'} passed;", s)
+    s = re.sub(r"same box \(`profiles/r02_v\d+_pytest_gpu\.log`: \d+ passed",
+               f"same box (`profiles/{tag}_pytest_gpu.log`: {n_pass.group(1) if n_pass else '?'} passed", s)
     open(p, "w").write(s)
 
 
