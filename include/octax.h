@@ -242,6 +242,25 @@ octax_status octax_set_state(octax_env *e, uint64_t env, const uint8_t *canon_in
 octax_status octax_state_digests(octax_env *e, uint64_t first, uint64_t count, uint64_t *digests_out,
                                  uint64_t *sum_out);
 
+/* Which step kernel runs the handle's launches (every entry point above; results identical,
+ * bit for bit -- both follow oracle/ c.1 and share the device state layout, so the choice may
+ * change between any two calls):
+ *   OCTAX_KERNEL_LANE -- one thread per env, 128 envs per CTA (the throughput kernel: the
+ *     GPU-filling batches of configs 3-5, 1M envs per GPU);
+ *   OCTAX_KERNEL_WARP -- one warp per env, the VM state in the warp's registers, no
+ *     divergence (the paper's lockstep bottleneck): lower latency per step, for batches
+ *     too small to fill the GPU with lane-per-env warps (512..8,192 envs);
+ *   OCTAX_KERNEL_AUTO -- WARP when n <= OCTAX_WARP_AUTO_MAX_ENVS (the measured crossover;
+ *     environment variable OCTAX_WARP_AUTO_MAX overrides it at create), else LANE.
+ * octax_set_kernel: OCTAX_E_INVALID_ARG for another value.  octax_get_kernel: the kernel in
+ * use (LANE or WARP), never AUTO. */
+#define OCTAX_KERNEL_AUTO 0
+#define OCTAX_KERNEL_LANE 1
+#define OCTAX_KERNEL_WARP 2
+#define OCTAX_WARP_AUTO_MAX_ENVS 4096
+octax_status octax_set_kernel(octax_env *e, int kernel);
+octax_status octax_get_kernel(octax_env *e, int *kernel_out);
+
 /* Handle facts: n_envs, n_actions, obs bytes per env, device bytes allocated. */
 octax_status octax_info(octax_env *e, uint64_t out4[4]);
 

@@ -504,7 +504,7 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   const uint64_t n = n_envs;
   size_t off = 0;
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
-  size_t o_img = carve(kStageBytes), o_dec = carve(8 * kDecEntries), o_stats = carve(64), o_regs = carve(16 * n), o_ctrl = carve(16 * n),
+  size_t o_img = carve(kStageBytes), o_dec = carve(8 * kDecEntries), o_words = carve(2 * kImageBytes), o_stats = carve(64), o_regs = carve(16 * n), o_ctrl = carve(16 * n),
          o_book = carve(16 * n), o_stack = carve(32 * n), o_dirty = carve(8 * n),
          o_ring = carve(1024 * ((n + kBlock - 1) / kBlock * kBlock)),
          o_ram = carve(4096 * n);
@@ -516,6 +516,7 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   uint8_t *base = (uint8_t *)e->block;
   p.s.image = base + o_img;
   p.s.dec = (const uint2 *)(base + o_dec);
+  p.s.words = (const uint16_t *)(base + o_words);
   p.s.stats = (unsigned long long *)(base + o_stats);
   p.s.regs = (uint4 *)(base + o_regs);
   p.s.ctrl = (uint4 *)(base + o_ctrl);
@@ -547,12 +548,18 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   ce = cudaMemcpyAsync(base + o_img, image, kStageBytes, cudaMemcpyHostToDevice, e->stream);
   if (ce == cudaSuccess)
     ce = cudaMemcpyAsync(base + o_dec, dec.data(), 8 * kDecEntries, cudaMemcpyHostToDevice, e->stream);
+  std::vector<uint16_t> words(kImageBytes, 0);
+  for (uint32_t pc = 0; pc < kImageBytes - 1; ++pc) words[pc] = (uint16_t)((image[pc] << 8) | image[pc + 1]);
+  words[kImageBytes - 1] = 0x5001;  // PC > 0xFFE (clamped to 0xFFF): an invalid word, the kernel halts (A17)
+  if (ce == cudaSuccess)
+    ce = cudaMemcpyAsync(base + o_words, words.data(), 2 * kImageBytes, cudaMemcpyHostToDevice, e->stream);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->stream);
   if (ce != cudaSuccess) { free_env(e); return cuda_err(ce, "upload image"); }
   if (e->obs_format != OCTAX_OBS_PACKED) {
     ce = cudaMalloc(&e->packed_scratch, 1024 * n);
     if (ce != cudaSuccess) { free_env(e); return cuda_err(ce, "cudaMalloc(obs scratch)"); }
   }
+  octax_set_kernel(e, OCTAX_KERNEL_AUTO);
   st = octax_reset(e, seed, nullptr);
   if (st != OCTAX_OK) { free_env(e); return st; }
   *out = e;
@@ -849,6 +856,25 @@ extern "C" octax_status octax_set_state(octax_env *e, uint64_t env, const uint8_
   CU(cudaMemcpyAsync(e->d_canon, canon_in, OCTAX_CANON_BYTES, cudaMemcpyHostToDevice, e->stream), "H2D canon");
   CU(launch_set_state(e->p, env, e->d_canon, e->stream), "set_state kernel");
   CU(cudaStreamSynchronize(e->stream), "sync");
+  return OCTAX_OK;
+}
+
+static uint64_t warp_auto_max() {
+  const char *s = getenv("OCTAX_WARP_AUTO_MAX");
+  return s ? strtoull(s, nullptr, 10) : (uint64_t)OCTAX_WARP_AUTO_MAX_ENVS;
+}
+
+extern "C" octax_status octax_set_kernel(octax_env *e, int kernel) {
+  if (!e) return set_err(OCTAX_E_INVALID_ARG, "NULL handle");
+  if (kernel != OCTAX_KERNEL_AUTO && kernel != OCTAX_KERNEL_LANE && kernel != OCTAX_KERNEL_WARP)
+    return set_err(OCTAX_E_INVALID_ARG, "kernel must be OCTAX_KERNEL_AUTO, _LANE or _WARP");
+  e->p.warp = kernel == OCTAX_KERNEL_WARP || (kernel == OCTAX_KERNEL_AUTO && e->n <= warp_auto_max());
+  return OCTAX_OK;
+}
+
+extern "C" octax_status octax_get_kernel(octax_env *e, int *kernel_out) {
+  if (!e || !kernel_out) return set_err(OCTAX_E_INVALID_ARG, "NULL argument");
+  *kernel_out = e->p.warp ? OCTAX_KERNEL_WARP : OCTAX_KERNEL_LANE;
   return OCTAX_OK;
 }
 

@@ -152,6 +152,8 @@ struct DevState {
   unsigned long long *stats;  // [4] {returns, episodes, steps, err}
   const uint8_t *image;       // [4096] pristine image: zeros, font at 0x50, ROM at 0x200
   const uint2 *dec;           // [kDecEntries] predecoded instruction at every PC (make_entry)
+  const uint16_t *words;      // [4096] the pristine image's 16-bit word at every PC <= 0xFFE
+                              // (warp-per-env kernel fetch: one load, no byte assembly)
 };
 
 struct StepParams {
@@ -177,6 +179,7 @@ struct StepParams {
   uint32_t stack_frames;  // OCTAX_OBS_STACK_FRAMES: obs = last 4 frames of the step
   uint32_t n_actions;     // n_action_keys + 1
   uint32_t n_startup;
+  uint32_t warp;          // 1: the warp-per-env kernel runs this launch (octax_set_kernel), 0: lane-per-env
   // fused rollout (MODE_ROLLOUT, octax_rollout): T steps per launch; step t's obs at obs + t *
   // obs_stride (u64 units), reward / done / terminated / truncated at [t * out_stride + env];
   // actions [T][n] if given, else generated in-kernel for step index t0 + t with key aseed

@@ -32,6 +32,7 @@
 // the CPU oracle in oracle/.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cassert>
 #include <cstdint>
@@ -1116,6 +1117,440 @@ reset_kernel(const __grid_constant__ StepParams p, uint8_t *__restrict__ obs) {
   }
 }
 
+// ---------------------------------------------------------------- warp-per-env kernel
+// One WARP interprets one environment (octax_set_kernel; auto below a few thousand envs).  The
+// lane-per-env kernel above is throughput-optimal when the GPU is full, but at the paper's own
+// env counts (512..8,192) it leaves most SMs idle and runs one warp per SM
+// sub-partition through a ~240-instruction predicated cycle: latency bound.
+// Here nothing diverges -- every lane follows the same env -- so each CHIP-8 instruction is a
+// warp-uniform switch case of a few instructions, and the VM state lives in registers:
+//   lane k < 16: V[k] (`v`) and return-stack entry k (`sk`); lane r: display row r (`fb`, one
+//   u64 in packed byte order); PC / I / SP / timers / keys / counters replicated in every lane.
+// DXYN is one row per lane (the "lanes of a warp cooperating on sprite rows" of the north star),
+// VF = a warp vote; FX55 / FX65 move register k in lane k.  RAM stays copy-on-write (64-B blocks
+// materialised in HBM on the first write, the pristine image read through L1).  Same state
+// layout, ring and outputs as the lane-per-env kernel, and the same semantics (oracle/ c.1):
+// the two are interchangeable on one handle between any two calls.
+#ifndef OCTAX_WCTA
+#define OCTAX_WCTA 4
+#endif
+constexpr int kWarpCta = OCTAX_WCTA;  // envs (warps) per CTA: small CTAs spread a small batch over all SMs
+
+struct WEnv {  // uniform per warp (replicated in every lane)
+  uint32_t pc, I, sp, dt, st, halted, draw, episode, keys;
+  uint64_t dirty;
+  uint8_t *ram;
+  const uint8_t *img;     // p.s.image, p.s.words: kept in registers (no constant-bank reloads)
+  const uint16_t *words;
+};
+
+// byte `a` (< 4096) of the env's memory: its HBM RAM block if written, else the pristine image.
+// RAM is written by this kernel, so it is read with plain loads (not the read-only path).
+__device__ __forceinline__ uint32_t w_rd(const StepParams &p, const WEnv &W, uint32_t a) {
+  OCTAX_CHECK(a < 4096u);
+  return ((W.dirty >> (a >> 6)) & 1ull) ? (uint32_t)W.ram[a] : (uint32_t)__ldg(W.img + a);
+}
+
+// lanes with `on` store byte `val` at their address `a` (< 4096; distinct per lane).  The 64-B
+// blocks any writer touches are materialised first (copy-on-write, 16 lanes x 4 B per block).
+__device__ __forceinline__ void w_wr(const StepParams &p, WEnv &W, int lane, bool on, uint32_t a, uint32_t val) {
+  OCTAX_CHECK(!on || a < 4096u);
+  const uint64_t need = on ? (1ull << (a >> 6)) : 0ull;
+  uint64_t m = ((uint64_t)__reduce_or_sync(kFull, (uint32_t)(need >> 32)) << 32) |
+               __reduce_or_sync(kFull, (uint32_t)need);
+  m &= ~W.dirty;
+  while (m) {
+    const uint32_t b = (uint32_t)__ffsll((long long)m) - 1u;
+    m &= m - 1;
+    if (lane < 16)
+      reinterpret_cast<uint32_t *>(W.ram + b * 64u)[lane] =
+          __ldg(reinterpret_cast<const uint32_t *>(W.img + b * 64u) + lane);
+    W.dirty |= 1ull << b;
+  }
+  __syncwarp();
+  if (on) W.ram[a] = (uint8_t)val;
+  __syncwarp();  // the bytes are visible to every lane's later reads
+}
+
+#define WV(k) __shfl_sync(kFull, v, (int)(k))
+
+// one CHIP-8 instruction (oracle/octax_oracle.c cycle(), readings A15-A23)
+__device__ __forceinline__ void w_cycle(const StepParams &p, WEnv &W, uint32_t &v, uint32_t &sk, uint64_t &fb,
+                                        int lane, uint32_t gid) {
+  const uint32_t pc = W.pc;
+  // the word at PC: one load, issued first, from the pristine word table (entry 0xFFF holds
+  // 0x5001, an invalid word, so a PC past 0xFFE lands on the halting path of class 5 below);
+  // re-assembled from RAM bytes when PC's 64-B block (or the next, holding PC + 1) was written
+  uint32_t op = __ldg(W.words + min(pc, 0xFFFu));
+  if (((W.dirty >> (pc >> 6)) & 3ull) != 0ull && pc <= 0xFFEu) op = (w_rd(p, W, pc) << 8) | w_rd(p, W, pc + 1u);
+  W.pc = pc + 2u;
+  const uint32_t x = (op >> 8) & 15u, y = (op >> 4) & 15u, n = op & 15u, nn = op & 255u, nnn = op & 0xFFFu;
+  const uint32_t quirks = p.quirks;
+  switch (op >> 12) {
+    case 0x0:
+      if (op == 0x00E0u) {
+        fb = 0;
+      } else if (op == 0x00EEu) {
+        if (W.sp == 0u) { W.halted = 1; return; }  // A20: stack underflow
+        W.sp -= 1u;
+        W.pc = __shfl_sync(kFull, sk, (int)W.sp);
+      }
+      break;  // other 0NNN: no-op (A20)
+    case 0x1: W.pc = nnn; break;
+    case 0x2:
+      if (W.sp == 16u) { W.halted = 1; return; }  // A20: stack overflow
+      sk = (uint32_t)lane == W.sp ? W.pc : sk;
+      W.sp += 1u;
+      W.pc = nnn;
+      break;
+    case 0x3: if (WV(x) == nn) W.pc += 2u; break;
+    case 0x4: if (WV(x) != nn) W.pc += 2u; break;
+    case 0x5:
+      if (n != 0u) {  // invalid word: halt with PC past it (A20); a fetch past 0xFFE: PC unchanged (A17)
+        W.halted = 1;
+        if (pc > 0xFFEu) W.pc = pc;
+        return;
+      }
+      if (WV(x) == WV(y)) W.pc += 2u;
+      break;
+    case 0x6: v = (uint32_t)lane == x ? nn : v; break;
+    case 0x7: v = (uint32_t)lane == x ? ((v + nn) & 255u) : v; break;  // VF untouched
+    case 0x8: {  // both operands read first, VF written last (A15)
+      const uint32_t a = WV(x), b = WV(y), s = (quirks & 1u) ? b : a;  // SHIFT_VY quirk
+      uint32_t r, f;
+      bool wf = true;
+      switch (n) {
+        case 0x0: r = b; wf = false; f = 0; break;
+        case 0x1: r = a | b; wf = (quirks & 16u) != 0u; f = 0; break;  // VF_RESET quirk
+        case 0x2: r = a & b; wf = (quirks & 16u) != 0u; f = 0; break;
+        case 0x3: r = a ^ b; wf = (quirks & 16u) != 0u; f = 0; break;
+        case 0x4: r = a + b; f = r >> 8; break;
+        case 0x5: r = a - b; f = a >= b; break;
+        case 0x6: r = s >> 1; f = s & 1u; break;
+        case 0x7: r = b - a; f = b >= a; break;
+        case 0xE: r = s << 1; f = (s >> 7) & 1u; break;
+        default: W.halted = 1; return;  // A20
+      }
+      v = (uint32_t)lane == x ? (r & 255u) : v;
+      if (wf) v = lane == 15 ? f : v;
+      break;
+    }
+    case 0x9:
+      if (n != 0u) { W.halted = 1; return; }
+      if (WV(x) != WV(y)) W.pc += 2u;
+      break;
+    case 0xA: W.I = nnn; break;
+    case 0xB: W.pc = (nnn + WV((quirks & 4u) ? x : 0u)) & 0xFFFu; break;  // JUMP_VX quirk
+    case 0xC: {  // A12: Philox(ctr = {draw, episode, gid, 0}, key = seed).out0 & NN
+      const uint32_t r = philox_out0(W.draw, W.episode, gid, 0u, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
+      v = (uint32_t)lane == x ? (r & nn) : v;
+      W.draw += 1u;
+      break;
+    }
+    case 0xD: {  // lane r draws display row r (sprite row (r - y0) & 31); A18 clip / WRAP quirk
+      const uint32_t x0 = WV(x) & 63u, y0 = WV(y) & 31u, base = W.I & 0xFFFu;
+      const bool wrap = (quirks & 8u) != 0u;
+      const uint32_t i = ((uint32_t)lane - y0) & 31u;
+      uint64_t mk = 0;
+      if (i < n && (wrap || (uint32_t)lane >= y0)) {
+        const uint32_t a = base + i;
+        const uint64_t nat = (uint64_t)(a <= 0xFFFu ? w_rd(p, W, a) : 0u) << 56;  // pixel c at bit 63 - c
+        const uint64_t m = (nat >> x0) | ((wrap && x0) ? nat << (64u - x0) : 0ull);
+        mk = bswap64(m);  // -> packed row byte order (byte b = pixels 8b..8b+7, MSB first)
+      }
+      const bool hit = __any_sync(kFull, (fb & mk) != 0ull);
+      fb ^= mk;
+      v = lane == 15 ? (uint32_t)hit : v;
+      break;
+    }
+    case 0xE: {
+      const bool down = ((W.keys >> (WV(x) & 15u)) & 1u) != 0u;  // A19
+      if (nn == 0x9Eu) { if (down) W.pc += 2u; }
+      else if (nn == 0xA1u) { if (!down) W.pc += 2u; }
+      else { W.halted = 1; return; }
+      break;
+    }
+    case 0xF:
+      switch (nn) {
+        case 0x07: v = (uint32_t)lane == x ? W.dt : v; break;
+        case 0x0A:  // A16: level-triggered wait (re-executes while no key is held)
+          if (W.keys) v = (uint32_t)lane == x ? (uint32_t)(__ffs((int)W.keys) - 1) : v;
+          else W.pc -= 2u;
+          break;
+        case 0x15: W.dt = WV(x); break;
+        case 0x18: W.st = WV(x); break;
+        case 0x1E: W.I = (W.I + WV(x)) & 0xFFFFu; break;
+        case 0x29: W.I = 0x50u + 5u * (WV(x) & 15u); break;
+        case 0x33: {  // BCD: lanes 0..2 store the three digits
+          const uint32_t vx = WV(x);
+          const uint32_t d = lane == 0 ? vx / 100u : lane == 1 ? (vx / 10u) % 10u : vx % 10u;
+          w_wr(p, W, lane, lane < 3, (W.I + (uint32_t)lane) & 0xFFFu, d);
+          break;
+        }
+        case 0x55:  // lane k <= x stores V[k]
+          w_wr(p, W, lane, (uint32_t)lane <= x, (W.I + (uint32_t)lane) & 0xFFFu, v);
+          if (quirks & 2u) W.I = (W.I + x + 1u) & 0xFFFFu;  // LOADSTORE_INC_I quirk
+          break;
+        case 0x65: {
+          const uint32_t a = (W.I + (uint32_t)(lane & 15)) & 0xFFFu;
+          const uint32_t b = w_rd(p, W, a);
+          v = (uint32_t)lane <= x ? b : v;
+          if (quirks & 2u) W.I = (W.I + x + 1u) & 0xFFFFu;
+          break;
+        }
+        default: W.halted = 1; return;
+      }
+      break;
+    default: __builtin_unreachable();
+  }
+}
+
+// one 60 Hz frame: ipf instructions, then the timer tick (A1, A2); halted envs stand still
+__device__ __forceinline__ void w_frame(const StepParams &p, WEnv &W, uint32_t &v, uint32_t &sk, uint64_t &fb,
+                                        int lane, uint32_t gid) {
+  for (uint32_t k = 0; k < p.ipf && !W.halted; ++k) w_cycle(p, W, v, sk, fb, lane, gid);
+  if (!W.halted) {
+    W.dt -= W.dt != 0u;
+    W.st -= W.st != 0u;
+  }
+}
+
+// score / termination program (same bytecode as eval(); V[k] from lane k)
+__device__ __forceinline__ uint32_t w_eval(const Program &P, const StepParams &p, const WEnv &W, uint32_t v) {
+  if (P.kind == 1u) return P.ka;
+  if (P.kind == 2u) return WV(P.ka);
+  if (P.kind == 3u) return WV(P.ka) == P.kb ? 1u : 0u;
+  if (P.kind == 4u) return WV(P.ka) != P.kb ? 1u : 0u;
+  uint32_t st[kMaxDepth];
+#pragma unroll
+  for (int k = 0; k < kMaxDepth; ++k) st[k] = 0;
+  for (uint32_t i = 0; i < P.len; ++i) {
+    const ExprInsn in = P.ops[i];
+    if (in.op <= X_VMOD) {
+      uint32_t val = in.op == X_CONST ? in.imm
+                   : in.op <= X_V || in.op >= X_VDIV ? WV(in.arg)
+                   : in.op == X_I  ? (W.I & 0xFFFFu)
+                   : in.op == X_DT ? W.dt : W.st;
+      if (in.op >= X_VDIV) {
+        const uint32_t q = (val * in.imm) >> 16;
+        val = in.op == X_VDIV ? q : val - q * (uint32_t)in.pad;
+      }
+#pragma unroll
+      for (int k = kMaxDepth - 1; k > 0; --k) st[k] = st[k - 1];
+      st[0] = val;
+    } else if (in.op < X_MUL) {
+      const uint32_t t = st[0];
+      st[0] = in.op == X_MEM ? w_rd(p, W, t & 0xFFFu) : in.op == X_NEG ? 0u - t : in.op == X_NOT ? (uint32_t)(t == 0u) : ~t;
+    } else {
+      const uint32_t a = st[1], b = st[0];
+      uint32_t r;
+      switch (in.op) {
+        case X_MUL: r = a * b; break;
+        case X_DIV: r = b ? a / b : 0u; break;
+        case X_MOD: r = b ? a % b : 0u; break;
+        case X_ADD: r = a + b; break;
+        case X_SUB: r = a - b; break;
+        case X_SHL: r = b >= 32u ? 0u : a << b; break;
+        case X_SHR: r = b >= 32u ? 0u : a >> b; break;
+        case X_LT: r = a < b; break;
+        case X_LE: r = a <= b; break;
+        case X_GT: r = a > b; break;
+        case X_GE: r = a >= b; break;
+        case X_EQ: r = a == b; break;
+        case X_NE: r = a != b; break;
+        case X_AND: r = a & b; break;
+        case X_XOR: r = a ^ b; break;
+        case X_OR: r = a | b; break;
+        case X_LAND: r = (a != 0u) & (b != 0u); break;
+        default: r = (a != 0u) | (b != 0u); break;
+      }
+#pragma unroll
+      for (int k = 1; k < kMaxDepth - 1; ++k) st[k] = st[k + 1];
+      st[kMaxDepth - 1] = 0;
+      st[0] = r;
+    }
+  }
+  return st[0];
+}
+
+// power-on + the spec's startup segments (A11); the new episode's score baseline
+__device__ __forceinline__ void w_reset(const StepParams &p, WEnv &W, uint32_t &v, uint32_t &sk, uint64_t &fb,
+                                        int lane, uint32_t gid, uint32_t &steps, uint32_t &prev, int32_t &ep_ret) {
+  v = 0; sk = 0; fb = 0;
+  W.pc = 0x200u; W.I = 0; W.sp = 0; W.dt = 0; W.st = 0; W.halted = 0; W.draw = 0; W.dirty = 0;
+  for (uint32_t seg = 0; seg < p.n_startup; ++seg) {
+    W.keys = p.startup_keys[seg];
+    for (uint32_t f = 0; f < p.startup_frames[seg]; ++f) w_frame(p, W, v, sk, fb, lane, gid);
+  }
+  W.keys = 0;
+  steps = 0;
+  prev = w_eval(p.score, p, W, v);
+  ep_ret = 0;
+}
+
+// <= 72 registers: 28+ resident warps (envs) per SM, so 4,096 envs run in one wave on 148 SMs
+// (at 95 registers a 4,096-env step took 1.36x longer: A/B); no spills at this cap
+template <int MODE>
+__global__ void __maxnreg__(72)
+octax_warp_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ actions, uint8_t *__restrict__ obs,
+                  float *__restrict__ reward, uint8_t *__restrict__ done_out, uint8_t *__restrict__ term_out,
+                  uint8_t *__restrict__ trunc_out) {
+  __shared__ unsigned long long red[4][kWarpCta];
+  const int lane = (int)(threadIdx.x & 31u), warp = (int)(threadIdx.x >> 5);
+  constexpr bool kRoll = MODE == MODE_ROLLOUT || MODE == MODE_ROLLOUT_NOOBS;
+  constexpr bool wobs = MODE != MODE_ROLLOUT_NOOBS;
+  // the launch covers envs [block_base * kBlock, ...) like the lane-per-env kernel's CTA blocks
+  const uint64_t e0 = (uint64_t)p.block_base * kBlock;
+  const uint64_t e1 = p.block_count ? min(p.n, e0 + (uint64_t)p.block_count * kBlock) : p.n;
+  const uint64_t env = e0 + (uint64_t)blockIdx.x * kWarpCta + (uint64_t)warp;
+  unsigned long long ret_acc = 0, finished = 0, nsteps = 0, err = 0;
+  if (env < e1) {  // uniform per warp
+    const uint32_t gid = (uint32_t)(p.env_offset + env), pos = (uint32_t)lane ^ ((uint32_t)env & kSwz);
+    uint64_t *obs64 = reinterpret_cast<uint64_t *>(obs);
+    WEnv W;
+    W.ram = p.s.ram + env * 4096ull;
+    W.img = p.s.image;
+    W.words = p.s.words;
+    asm volatile("" : "+l"(W.img), "+l"(W.words));  // kept in registers, not re-read per cycle
+    W.keys = 0;
+    uint32_t v = 0, sk = 0, steps = 0, prev = 0;
+    int32_t ep_ret = 0;
+    uint64_t fb = 0, hA = 0, hB = 0;  // display (row `lane`); ends of steps t-3, t-2 (obs planes 0, 1)
+    if (MODE == MODE_RESET) {
+      W.episode = 0;
+      w_reset(p, W, v, sk, fb, lane, gid, steps, prev, ep_ret);
+      for (uint32_t sl = 0; sl < 4; ++sl) ring_at(p, sl, env)[pos] = fb;
+      if (obs64)
+        for (uint32_t pl = 0; pl < 4; ++pl) __stcs(obs64 + env * 128 + pl * 32 + lane, fb);
+    } else {
+      const uint4 r = p.s.regs[env];
+      const uint32_t k = (uint32_t)lane & 15u, w = k < 4u ? r.x : k < 8u ? r.y : k < 12u ? r.z : r.w;
+      v = (w >> (8u * (k & 3u))) & 255u;
+      const uint4 c = p.s.ctrl[env];
+      W.pc = c.x & 0xFFFFu; W.I = c.x >> 16;
+      W.sp = c.y & 255u; W.dt = (c.y >> 8) & 255u; W.st = (c.y >> 16) & 255u; W.halted = c.y >> 24;
+      W.draw = c.z; W.episode = c.w;
+      const uint4 b = p.s.book[env];
+      steps = b.x; prev = b.y; ep_ret = (int32_t)b.z;
+      sk = reinterpret_cast<const uint16_t *>(p.s.stack)[env * 16u + k];
+      W.dirty = p.s.dirty[env];
+      fb = ring_at(p, p.head & 3u, env)[pos];
+      hA = ring_at(p, (p.head + 2u) & 3u, env)[pos];
+      hB = ring_at(p, (p.head + 3u) & 3u, env)[pos];
+      const uint32_t T = kRoll ? p.T : 1u;
+      const bool sf = p.stack_frames != 0u;
+      for (uint32_t t = 0; t < T; ++t) {
+        const uint32_t h = (p.head + t) & 3u;
+        uint64_t *ob = obs64 ? obs64 + (kRoll ? t * p.obs_stride : 0u) + env * 128 : nullptr;
+        const uint64_t oo = kRoll ? t * p.out_stride : 0u;
+        int32_t a;
+        if (!kRoll) a = actions[env];
+        else if (actions) a = actions[t * p.n + env];
+        else {
+          const uint64_t ts = p.t0 + t;
+          a = (int32_t)(philox_out0((uint32_t)ts, (uint32_t)(ts >> 32), gid, 1u, (uint32_t)p.aseed,
+                                    (uint32_t)(p.aseed >> 32)) % p.n_actions);
+        }
+        if (a < 0 || (uint32_t)a >= p.n_actions) {  // out of range: no-op + sticky flag
+          a = 0;
+          err = 1;
+        }
+        W.keys = p.keymask[a];
+        const uint64_t start = fb;
+        // obs planes 0..2: the last step-end displays, or (stack_frames) the displays after the
+        // last frames of this step, planes before the step's first frame = step-start display
+        uint64_t P0 = sf ? start : hA, P1 = sf ? start : hB, P2 = start;
+        for (uint32_t f = 0; f < p.frame_skip; ++f) {
+          w_frame(p, W, v, sk, fb, lane, gid);
+          const int pl = (int)f + 4 - (int)p.frame_skip;
+          if (sf) {
+            P0 = pl == 0 ? fb : P0;
+            P1 = pl == 1 ? fb : P1;
+            P2 = pl == 2 ? fb : P2;
+          }
+        }
+        const uint32_t s = w_eval(p.score, p, W, v);
+        const int32_t d = (int32_t)(s - prev);
+        prev = s;
+        ep_ret = (int32_t)((uint32_t)ep_ret + (uint32_t)d);
+        steps++;
+        const uint32_t term = (w_eval(p.term, p, W, v) != 0u) || W.halted;
+        const uint32_t trunc = p.max_steps && steps >= p.max_steps;
+        const uint32_t done = term | trunc;
+        if (lane == 0) {
+          reward[oo + env] = (float)d;
+          done_out[oo + env] = (uint8_t)done;
+          if (term_out) term_out[oo + env] = (uint8_t)term;
+          if (trunc_out) trunc_out[oo + env] = (uint8_t)trunc;
+          if (p.ep_ret_out) p.ep_ret_out[env] = done ? ep_ret : 0;
+          if (p.ep_len_out) p.ep_len_out[env] = done ? steps : 0u;
+        }
+        nsteps++;
+        if (done) {
+          if (p.final_obs) {
+            uint64_t *fo = reinterpret_cast<uint64_t *>(p.final_obs) + env * 128 + lane;
+            fo[0] = P0; fo[32] = P1; fo[64] = P2; fo[96] = fb;
+          }
+          ret_acc += (unsigned long long)(long long)ep_ret;
+          finished++;
+          W.episode++;
+          w_reset(p, W, v, sk, fb, lane, gid, steps, prev, ep_ret);  // A10: same-step auto-reset
+          P0 = P1 = P2 = fb;
+          for (uint32_t sl = 0; sl < 4; ++sl) ring_at(p, sl, env)[pos] = fb;
+          hA = hB = fb;
+        } else {
+          ring_at(p, (h + 1u) & 3u, env)[pos] = fb;
+          hA = hB;
+          hB = start;
+        }
+        if (wobs && ob) {
+          __stcs(ob + lane, P0);
+          __stcs(ob + 32 + lane, P1);
+          __stcs(ob + 64 + lane, P2);
+          __stcs(ob + 96 + lane, fb);
+        }
+        if (MODE == MODE_STEP && p.frame_out) __stcs(reinterpret_cast<uint64_t *>(p.frame_out) + env * 32 + lane, fb);
+      }
+    }
+    // store the VM state (same layout as the lane-per-env kernel)
+    if (lane < 16) {
+      reinterpret_cast<uint8_t *>(p.s.regs + env)[lane] = (uint8_t)v;
+      reinterpret_cast<uint16_t *>(p.s.stack)[env * 16u + (uint32_t)lane] = (uint16_t)sk;
+    }
+    if (lane == 0) {
+      p.s.ctrl[env] = make_uint4((W.pc & 0xFFFFu) | (W.I << 16), W.sp | (W.dt << 8) | (W.st << 16) | (W.halted << 24),
+                                 W.draw, W.episode);
+      p.s.book[env] = make_uint4(steps, prev, (uint32_t)ep_ret, 0u);
+      p.s.dirty[env] = W.dirty;
+    }
+  }
+  // integer episode statistics (a12): per CTA, 4 atomics
+  if (MODE != MODE_RESET) {
+    if (lane == 0) { red[0][warp] = ret_acc; red[1][warp] = finished; red[2][warp] = nsteps; red[3][warp] = err; }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+      unsigned long long acc = 0;
+      for (int w2 = 0; w2 < kWarpCta; ++w2) acc = threadIdx.x == 3 ? (acc | red[3][w2]) : acc + red[threadIdx.x][w2];
+      if (acc) {
+        if (threadIdx.x == 3) atomicOr(&p.s.stats[3], acc);
+        else atomicAdd(&p.s.stats[threadIdx.x], acc);
+      }
+    }
+  }
+}
+#undef WV
+
+template <int MODE>
+static cudaError_t launch_warp(const StepParams &p, const int32_t *actions, uint8_t *obs, float *reward, uint8_t *done,
+                               uint8_t *term, uint8_t *trunc, cudaStream_t stream) {
+  const uint64_t e0 = (uint64_t)p.block_base * kBlock;
+  const uint64_t e1 = p.block_count ? std::min<uint64_t>(p.n, e0 + (uint64_t)p.block_count * kBlock) : p.n;
+  if (e1 <= e0) return cudaSuccess;
+  const unsigned grid = (unsigned)((e1 - e0 + kWarpCta - 1) / kWarpCta);
+  octax_warp_kernel<MODE><<<grid, 32 * kWarpCta, 0, stream>>>(p, actions, obs, reward, done, term, trunc);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- auxiliary kernels
 __global__ void gen_actions_kernel(uint64_t n, uint64_t env_offset, uint64_t aseed, uint64_t t,
                                    uint32_t n_actions, int32_t *__restrict__ out) {
@@ -1280,6 +1715,13 @@ static cudaError_t launch_resets(const StepParams &p, uint8_t *obs, cudaStream_t
 
 cudaError_t launch_step(const StepParams &p, int mode, const int32_t *actions, uint8_t *obs, float *reward,
                         uint8_t *done, uint8_t *term, uint8_t *trunc, cudaStream_t stream) {
+  if (p.warp) {  // warp-per-env kernel: every mode, resets inline (no reset_kernel)
+    if (mode == MODE_STEP) return launch_warp<MODE_STEP>(p, actions, obs, reward, done, term, trunc, stream);
+    if (mode == MODE_ROLLOUT)
+      return obs ? launch_warp<MODE_ROLLOUT>(p, actions, obs, reward, done, term, trunc, stream)
+                 : launch_warp<MODE_ROLLOUT_NOOBS>(p, actions, obs, reward, done, term, trunc, stream);
+    return launch_warp<MODE_RESET>(p, nullptr, obs, nullptr, nullptr, nullptr, nullptr, stream);
+  }
   const bool q0 = p.quirks == 0u;
   if (mode == MODE_STEP) {
     if (p.reset_ids) {  // deferred resets: count from zero, step, then the listed resets

@@ -26,8 +26,11 @@ OBS_STACK_FRAMES = 16
 SYMBOLS = (
     "octax_create", "octax_reset", "octax_step", "octax_step_ex", "octax_step_host", "octax_step_host_frame", "octax_rollout", "octax_gen_actions",
     "octax_stats", "octax_stats_device", "octax_get_state", "octax_get_states",
-    "octax_set_state", "octax_state_digests", "octax_info", "octax_destroy", "octax_last_error",
+    "octax_set_state", "octax_state_digests", "octax_set_kernel", "octax_get_kernel", "octax_info",
+    "octax_destroy", "octax_last_error",
 )
+# octax_set_kernel values (include/octax.h OCTAX_KERNEL_*)
+KERNELS = {"auto": 0, "lane": 1, "warp": 2}
 
 
 class OctaxError(RuntimeError):
@@ -94,6 +97,8 @@ def load_library():
     L.octax_get_states.argtypes = [P, P, u64, P]
     L.octax_set_state.argtypes = [P, u64, P]
     L.octax_state_digests.argtypes = [P, u64, u64, P, P]
+    L.octax_set_kernel.argtypes = [P, ctypes.c_int]
+    L.octax_get_kernel.argtypes = [P, P]
     L.octax_info.argtypes = [P, P]
     L.octax_destroy.argtypes = [P]
     L.octax_destroy.restype = None
@@ -147,10 +152,12 @@ class OctaxEnv:
 
     ``step(actions)`` -> (obs, reward, done) as torch CUDA tensors owned by this
     object (overwritten by the next step); ``step_into`` writes caller buffers.
+    ``kernel``: "auto" (default; environment variable OCTAX_KERNEL overrides), "lane" or
+    "warp" -- which step kernel runs the launches (octax_set_kernel; identical results).
     """
 
     def __init__(self, rom: bytes, spec: dict, n_envs: int, seed: int, device: int = 0,
-                 env_offset: int = 0, total_envs: int = 0, stream=None):
+                 env_offset: int = 0, total_envs: int = 0, stream=None, kernel: str | None = None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("OctaxEnv needs a CUDA device (no CPU fallback)")
@@ -169,6 +176,12 @@ class OctaxEnv:
         _check(L.octax_create(rom_arr, len(rom), ctypes.byref(cs), self.n, seed & (2**64 - 1),
                               ctypes.byref(opts), ctypes.byref(h)))
         self._h = h
+        kernel = kernel or os.environ.get("OCTAX_KERNEL", "auto")
+        if kernel != "auto":
+            auto = self.kernel
+            self.set_kernel(kernel)
+            if self.kernel != auto:  # the initial reset again, by the chosen kernel (same state)
+                _check(L.octax_reset(self._h, seed & (2**64 - 1), None))
         shape = (self.n, 4, 32, 8) if self.obs_format == OBS_PACKED else (self.n, 4, 64, 32)
         self.obs = torch.zeros(shape, dtype=torch.uint8, device=self.device)
         self.reward = torch.zeros(self.n, dtype=torch.float32, device=self.device)
@@ -300,6 +313,17 @@ class OctaxEnv:
         _check(load_library().octax_state_digests(self._h, first, n, ctypes.c_void_p(out.ctypes.data),
                                                   ctypes.c_void_p(tot.ctypes.data)))
         return out, int(tot[0])
+
+    def set_kernel(self, kernel: str) -> None:
+        if kernel not in KERNELS:
+            raise ValueError(f"kernel must be one of {sorted(KERNELS)}")
+        _check(load_library().octax_set_kernel(self._h, KERNELS[kernel]))
+
+    @property
+    def kernel(self) -> str:
+        k = ctypes.c_int(0)
+        _check(load_library().octax_get_kernel(self._h, ctypes.byref(k)))
+        return {1: "lane", 2: "warp"}[k.value]
 
     def info(self):
         out = np.zeros(4, np.uint64)

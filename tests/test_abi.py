@@ -110,3 +110,15 @@ def test_null_arguments_new_entry_points(lib):
     assert lib.octax_rollout(None, 4, None, 0, 0, None, 0, None, None, None, None, 0) == -1
     assert lib.octax_step_host_frame(None, None, None, None, None, None, None) == -1
     assert lib.octax_step_host(None, None, None, None, None, None, None) == -1
+
+
+def test_kernel_selection_rejects_null_and_bad_values(lib):
+    """octax_set_kernel / octax_get_kernel (include/octax.h): NULL handle or output refused on the
+    host; the three OCTAX_KERNEL_* values are the binding's KERNELS table."""
+    from paper_2510_01764_b200.octax import KERNELS
+    assert lib.octax_set_kernel(None, 0) == -1
+    k = ctypes.c_int(0)
+    assert lib.octax_get_kernel(None, ctypes.byref(k)) == -1
+    hdr = open(os.path.join(ROOT, "include", "octax.h")).read()
+    for name, val in KERNELS.items():
+        assert f"#define OCTAX_KERNEL_{name.upper()} {val}" in hdr
