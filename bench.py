@@ -221,14 +221,14 @@ def run_reference(args):
 
 # ------------------------------------------------------------------ GPU arm
 def time_config(rom, spec, n, steps, warmup, rank_offset, aseed, torch, OctaxEnv, barrier=None,
-                keep=False, graph=False, rollout=0, on_rollout=None):
+                keep=False, graph=False, rollout=0, on_rollout=None, kernel=None):
     """Time `steps` octax_step launches (each = one step of all n envs) on a dedicated
     stream with CUDA events; graph=True captures the K launches in one CUDA graph
     (K % 4 == 0 keeps the 4-slot display ring aligned across replays).  on_rollout(env, stream)
     runs inside the timed region after every `rollout` steps and after the last one (the
     per-rollout statistics all-reduce of SURVEY §8(e))."""
     stream = torch.cuda.Stream()
-    env = OctaxEnv(rom, spec, n, 0x0C7A251001764000, env_offset=rank_offset, stream=stream)
+    env = OctaxEnv(rom, spec, n, 0x0C7A251001764000, env_offset=rank_offset, stream=stream, kernel=kernel)
     T = warmup + steps
     acts = torch.empty((T, n), dtype=torch.int32, device="cuda")
     with torch.cuda.stream(stream):
@@ -276,7 +276,7 @@ def time_config(rom, spec, n, steps, warmup, rank_offset, aseed, torch, OctaxEnv
 
 
 def time_rollout(rom, spec, n, T, reps, warmup_reps, rank_offset, aseed, torch, OctaxEnv, barrier=None,
-                 on_rollout=None, with_obs=True):
+                 on_rollout=None, with_obs=True, kernel=None):
     """Fused rollout mode (octax_rollout, SURVEY d.8 mode "fused"): `reps` launches of T steps
     each, actions generated inside the kernel (the step mode's actions are generated before its
     timed region, so this mode does strictly more work per step), obs / reward / done written
@@ -284,7 +284,7 @@ def time_rollout(rom, spec, n, T, reps, warmup_reps, rank_offset, aseed, torch, 
     on_rollout(env, stream) after every rollout inside the timed region.  Returns
     (total_ms, per-rollout ms, env)."""
     stream = torch.cuda.Stream()
-    env = OctaxEnv(rom, spec, n, 0x0C7A251001764000, env_offset=rank_offset, stream=stream)
+    env = OctaxEnv(rom, spec, n, 0x0C7A251001764000, env_offset=rank_offset, stream=stream, kernel=kernel)
     obs, rew, done = env.obs if with_obs else None, env.reward, env.done
     t = 0
     with torch.cuda.stream(stream):
@@ -627,12 +627,26 @@ def main():
             row["frames_per_s_graph"] = 4 * row["steps_per_s_graph"]
             tm, _, fenv = time_rollout(rom, spec, m, 100, 2, 1, odist.shard(rank, world, m)[0],
                                        workloads.ACTION_SEED, torch, OctaxEnv, barrier)
+            row["kernel"] = fenv.kernel  # OCTAX_KERNEL_AUTO's choice for this batch size
             fenv.close()
             tt = float(odist.max_over_ranks(torch.tensor([tm], dtype=torch.float64, device="cuda")).item())
             row["steps_per_s_fused"] = world * m * 200 / (tt / 1e3)
             row["ms_per_step_fused"] = tt / 200
+            if row["kernel"] == "warp":  # the lane-per-env kernel on the same batch, for comparison
+                lk = {}
+                tm, _, _ = time_config(rom, spec, m, ks, args.warmup, odist.shard(rank, world, m)[0],
+                                       workloads.ACTION_SEED, torch, OctaxEnv, barrier, kernel="lane")
+                tt = float(odist.max_over_ranks(torch.tensor([tm], dtype=torch.float64, device="cuda")).item())
+                lk["steps_per_s_launch"] = world * m * ks / (tt / 1e3)
+                tm, _, fenv = time_rollout(rom, spec, m, 100, 2, 1, odist.shard(rank, world, m)[0],
+                                           workloads.ACTION_SEED, torch, OctaxEnv, barrier, kernel="lane")
+                fenv.close()
+                tt = float(odist.max_over_ranks(torch.tensor([tm], dtype=torch.float64, device="cuda")).item())
+                lk["steps_per_s_fused"] = world * m * 200 / (tt / 1e3)
+                row["lane_kernel"] = lk
             sweep.append(row)
-        sweep.append({"envs_per_gpu": n, "steps_per_s_launch": value, "frames_per_s_launch": 4 * value,
+        sweep.append({"envs_per_gpu": n, "kernel": "lane" if n > int(os.environ.get("OCTAX_WARP_AUTO_MAX", 4096)) else "warp",
+                      "steps_per_s_launch": value, "frames_per_s_launch": 4 * value,
                       "ms_per_step_launch": t_max / args.steps,
                       **({"steps_per_s_fused": fused["steps_per_s"], "ms_per_step_fused": fused["ms_per_step"]}
                          if fused else {})})

@@ -46,6 +46,10 @@ def main():
             j["envs_per_launch"] = 1048576
             for out in (f"{tag}_fused_full_1048576.json", "latest_fused_full.json"):
                 json.dump(j, open(os.path.join(P, out), "w"), indent=1)
+    for f in sorted(glob.glob(os.path.join(G, "warp_full_*.json"))):  # warp-per-env kernel captures
+        if json.load(open(f)).get("sass_sha256") == have:
+            shutil.copy(f, os.path.join(P, f"{tag}_{os.path.basename(f)}"))
+            caps.append(os.path.join(P, f"{tag}_{os.path.basename(f)}"))
     order = [c for c in caps if c.endswith("_full_1048576.json")] + \
             [c for c in caps if c.endswith("_full_262144.json")] + \
             [c for c in caps if not c.endswith(("_full_1048576.json", "_full_262144.json"))]
@@ -56,6 +60,10 @@ def main():
     if os.path.exists(os.path.join(G, "fused_1048576.ncu-rep")):
         run("scripts/ncu_source.py", os.path.join(G, "fused_1048576.ncu-rep"),
             os.path.join(P, f"{tag}_fused_source_attr_1M.md"), "--envs", "104857600", "--kernel", "octax_kernel<(int)2")
+    wrep = os.path.join(G, "warp_full_pong_standin_4096.ncu-rep")
+    if os.path.exists(wrep):
+        run("scripts/ncu_source.py", wrep, os.path.join(P, f"{tag}_warp_source_attr_4096.md"), "--envs", "4096",
+            "--kernel", "octax_warp_kernel")
     if os.path.exists(os.path.join(G, "launches.csv")):
         run("scripts/ncu_summary.py", "launches", os.path.join(G, "launches.csv"), os.path.join(P, f"{tag}_launches.md"))
     for src, dst in (("paper_protocol.json", "paper_protocol.json"), ("paper_protocol.md", "paper_protocol.md"),

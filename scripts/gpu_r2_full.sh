@@ -30,6 +30,15 @@ for G in ${NCU_GAMES:-brix_standin target_shooter_level1 target_shooter_level2 t
   echo "ncu $TAG rc=$?"
   python scripts/ncu_summary.py full gpurun_out/$TAG.ncu-rep gpurun_out/step_$TAG.json --envs 262144 --game $G --so $SO > /dev/null 2>&1
 done
+# the warp-per-env kernel (OCTAX_KERNEL_AUTO at n <= 4,096): configs[1]'s 4,096-env step
+for G in ${WARP_GAMES:-pong_standin target_shooter_level3}; do
+  TAG=warp_full_${G}_4096
+  PCMD="python bench.py --steps 3 --warmup 3 --envs 4096 --game $G --no-sweep --no-e2e --no-cpu --no-fused"
+  timeout 300 $PCMD > gpurun_out/plain_$TAG.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:octax_warp_kernel -s 5 -c 1 -o gpurun_out/$TAG -f $PCMD > gpurun_out/ncu_$TAG.log 2>&1
+  echo "ncu $TAG rc=$?"
+  python scripts/ncu_summary.py full gpurun_out/$TAG.ncu-rep gpurun_out/$TAG.json --envs 4096 --game $G --so $SO > /dev/null 2>&1
+done
 if [ -n "$FUSED_NCU" ]; then  # one 100-step fused rollout launch (octax_kernel<2,1>) at 1M envs
   PCMD="python bench.py --steps 3 --warmup 3 --envs 1048576 --no-sweep --no-e2e --no-cpu"
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:octax_kernel -s 8 -c 1 \

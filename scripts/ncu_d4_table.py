@@ -32,7 +32,8 @@ ROWS = [
 def main():
     out, files = sys.argv[1], sys.argv[2:]
     caps = [json.load(open(f)) for f in files]
-    hdr = "| metric (ncu name) | " + " | ".join(f"{c.get('game')} @ {c.get('envs'):,} envs" for c in caps) + " |"
+    kind = lambda c: " (warp-per-env)" if "warp_kernel" in str(c.get("kernel_symbol")) else ""  # noqa: E731
+    hdr = "| metric (ncu name) | " + " | ".join(f"{c.get('game')} @ {c.get('envs'):,} envs{kind(c)}" for c in caps) + " |"
     lines = [hdr, "|---" * (len(caps) + 1) + "|"]
     for label, m, scale in ROWS:
         cells = []

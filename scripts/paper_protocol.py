@@ -101,9 +101,10 @@ def rollouts(game, n, obs_format, mode, reps, T=100, warm=0, launch="step"):
         if r > 0:  # first rollout is the warm-up
             times.append(e0.elapsed_time(e1) / 1e3)
     del g
+    kernel = env.kernel  # OCTAX_KERNEL_AUTO's choice: warp-per-env for n <= 4,096
     env.close()
     sps = np.array([n * T / t for t in times])
-    return float(np.median(sps)), float(np.percentile(sps, 75) - np.percentile(sps, 25))
+    return float(np.median(sps)), float(np.percentile(sps, 75) - np.percentile(sps, 25)), kernel
 
 
 # SURVEY d.8 "bitexact, n_envs_checked, steps_checked": the GPU parity test that covers each
@@ -111,7 +112,8 @@ def rollouts(game, n, obs_format, mode, reps, T=100, warm=0, launch="step"):
 # of the same box run, gpurun_out/pytest_gpu.log, when present)
 BITEXACT = {
     "1": ("tests/test_gpu_parity.py::test_coverage_rom_n1_1000_steps_full_state_every_step", 1, 1000),
-    "2": ("tests/test_gpu_rollout.py::test_rollout_equals_steps_on_gpu_at_4096 + test_game_parity[pong_standin-300]", 300, 300),
+    "2": ("tests/test_gpu_kernels.py::test_config2_pong_4096_sampled_parity (every env, warp kernel as AUTO runs it) + "
+          "tests/test_gpu_rollout.py::test_rollout_equals_steps_on_gpu_at_4096", 4096, 200),
     "2*": ("tests/test_gpu_parity.py::test_game_parity[pong_standin-300]", 300, 300),
     "3": ("tests/test_gpu_parity.py::test_game_parity[brix_standin-257] + test_bool_obs_startup_and_truncation_parity", 257, 300),
     "4": ("tests/test_gpu_parity.py::test_config4_sampled_parity_1000_steps (64 sampled envs per game)", 64, 1000),
@@ -133,18 +135,20 @@ def pytest_status(tests: str):
     return "FAIL: " + ", ".join(bad) if bad else "pass"
 
 
-def ncu_model(game, n):
+def ncu_model(game, n, kernel="lane"):
     """I_step, ALU-pipe instructions, eta and DRAM bytes per env step from an ncu capture of THIS
-    build (device-code digest) for this game: the one at this env count if there is one, else the
-    game's capture at another count (instructions per env step do not depend on n: 363.2 at 1M vs
-    363.3 at 262K for kernel v35; DRAM bytes do, below ~1e5 envs the state stays in L2)."""
+    build (device-code digest) of the kernel that ran the row (lane-per-env: step_full*.json;
+    warp-per-env: warp_full*.json) for this game: the one at this env count if there is one, else
+    the game's capture at another count (instructions per env step do not depend on n: 363.2 at 1M
+    vs 363.3 at 262K for kernel v35; DRAM bytes do, below ~1e5 envs the state stays in L2)."""
     import glob
     from paper_2510_01764_b200 import octax
     from paper_2510_01764_b200.build import device_code_digest
     have = device_code_digest(octax.SO_PATH)
     caps = []
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*step_full*.json")) +
-                    glob.glob(os.path.join(ROOT, "gpurun_out", "step_full*.json"))):
+    pat = "warp_full" if kernel == "warp" else "step_full"
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", f"*{pat}*.json")) +
+                    glob.glob(os.path.join(ROOT, "gpurun_out", f"{pat}*.json"))):
         try:
             j = json.load(open(f))
         except Exception:
@@ -202,12 +206,12 @@ def main():
         jobs += [(cid, game, n, fmt, mode, warm, ln) for ln in launches]
     for cid, game, n, fmt, mode, warm, launch in jobs:
         with ClockSampler(0) as clk:
-            med, iqr = rollouts(game, n, fmt, mode, args.reps, warm=warm, launch=launch)
+            med, iqr, kernel = rollouts(game, n, fmt, mode, args.reps, warm=warm, launch=launch)
         ck = clk.summary()
         f_sm = (ck["sm_mhz"] or 1965.0) * 1e6
         rom, spec = workloads.game(game)
         cyc = spec["frame_skip"] * spec["instructions_per_frame"]
-        nm = ncu_model(game, n) if fmt == 0 else None  # fused: the step kernel's counts (an upper bound)
+        nm = ncu_model(game, n, kernel) if fmt == 0 else None  # fused: the step kernel's counts (an upper bound)
         # SURVEY d.2 roofs: issue = 148 SMs x 4 schedulers x 1 warp instr / cycle; ALU pipe = 148 x 4 x
         # 1 warp instr / 2 cycles; each / the measured warp instructions per env step
         R_issue = 148 * 4 * f_sm / nm["I_step_warp"] if nm and nm["I_step_warp"] else None
@@ -221,7 +225,7 @@ def main():
         if launch == "fused":
             bt += (" + tests/test_gpu_rollout.py (test_rollout_games_parity, test_rollout_generated_actions_parity, "
                    "test_rollout_equals_steps_on_gpu_at_4096, test_rollout_1M_sampled_parity_and_step_equivalence)")
-        row = {"config": cid, "game": game, "rom": rom_label(game, rom), "envs": n, "gpus": 1,
+        row = {"config": cid, "game": game, "rom": rom_label(game, rom), "envs": n, "gpus": 1, "kernel": kernel,
                "obs": "bool" if fmt else "packed", "mode": launch, "actions": mode,
                "protocol": "mixed" if warm else "fresh", "warmup_steps": warm + 100,
                "steps_per_rollout": 100, "reps": args.reps,
@@ -251,13 +255,13 @@ def main():
     with open(args.out + ".json", "w") as f:
         json.dump({"device": dev, "protocol": "P:228, 1 warm-up + %d x 100-step rollouts" % args.reps,
                    "rows": rows}, f, indent=1)
-    lines = ["| config | game | envs | obs | mode | actions | protocol | steps/s median | IQR | frames/s | SM MHz | "
+    lines = ["| config | game | envs | kernel | obs | mode | actions | protocol | steps/s median | IQR | frames/s | SM MHz | "
              "binding roof (frac) | bitexact (envs x steps) | oracle 1 core | oracle all cores (C) |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         roof = f"{r['binding']} ({r['frac_binding']:.2f})" if r["binding"] else "-"
         mode = r["mode"] + (" (bool expanded for the last step)" if r.get("obs_note") else "")
-        lines.append(f"| {r['config']} | {r['game']} | {r['envs']:,} | {r['obs']} | {mode} | {r['actions']} | "
+        lines.append(f"| {r['config']} | {r['game']} | {r['envs']:,} | {r['kernel']} | {r['obs']} | {mode} | {r['actions']} | "
                      f"{r['protocol']} | {r['steps_per_s_median']:.4g} | {r['steps_per_s_iqr']:.3g} | "
                      f"{r['frames_per_s_median']:.4g} | {r['sm_clock_mhz_during']} | {roof} | "
                      f"{r['bitexact']} ({r['n_envs_checked']} x {r['steps_checked']}) | "
@@ -266,8 +270,9 @@ def main():
         f.write(f"# Paper protocol (P:228) on {dev}, host CPU {cpu_model}\n\n1 warm-up + {args.reps} timed 100-step "
                 "rollouts per row; CUDA events; device-resident actions (fused: generated in the kernel).  Modes "
                 "(SURVEY d.8): step = 100 octax_step launches, graph = the same launches in one CUDA graph, "
-                "fused = one octax_rollout launch.  Roofs (SURVEY d.2): issue / ALU pipe from the ncu capture of "
-                "this build at the row's game and env count, HBM from 2,201 algorithmic B per env step; "
+                "fused = one octax_rollout launch.  Kernel = OCTAX_KERNEL_AUTO's choice (warp-per-env for n <= "
+                "4,096, lane-per-env above).  Roofs (SURVEY d.2): issue / ALU pipe from the ncu capture of "
+                "this build's kernel at the row's game and env count, HBM from 2,201 algorithmic B per env step; "
                 "the full d.8 row is in the .json.\n\n" + "\n".join(lines) + "\n")
     print("\n".join(lines))
 

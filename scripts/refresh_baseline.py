@@ -17,18 +17,18 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def table(tag):
     rows = json.load(open(os.path.join(ROOT, "profiles", f"{tag}_paper_protocol.json")))["rows"]
-    key = lambda r: (r["config"], r["game"], r["envs"], r["obs"], r["actions"], r["protocol"])  # noqa: E731
+    key = lambda r: (r["config"], r["game"], r["envs"], r["obs"], r["actions"], r["protocol"], r.get("kernel", "lane"))  # noqa: E731
     g = collections.OrderedDict()
     for r in rows:
         g.setdefault(key(r), {})[r["mode"]] = r
     f = lambda x: f"{x:.3g}"  # noqa: E731
     b = lambda r: f"{r['binding']} ({r['frac_binding']:.2f})" if r and r["binding"] else "—"  # noqa: E731
-    out = ["| Config | Game / ROM | n per GPU | Obs | Actions | Protocol | step: steps/s (IQR) | CUDA graph | "
+    out = ["| Config | Game / ROM | n per GPU | Kernel | Obs | Actions | Protocol | step: steps/s (IQR) | CUDA graph | "
            "fused (`octax_rollout`) | binding roof, step (frac) | binding roof, fused (frac) | Oracle 1 core | "
-           "Oracle 16 cores |", "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+           "Oracle 16 cores |", "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for k, m in g.items():
         st, gr, fu = m["step"], m.get("graph"), m.get("fused")
-        out.append(f"| {k[0]} | {k[1]} | {k[2]:,} | {k[3]} | {k[4]} | {k[5]} | {f(st['steps_per_s_median'])} "
+        out.append(f"| {k[0]} | {k[1]} | {k[2]:,} | {k[6]} | {k[3]} | {k[4]} | {k[5]} | {f(st['steps_per_s_median'])} "
                    f"({f(st['steps_per_s_iqr'])}) | {f(gr['steps_per_s_median']) if gr else '—'} | "
                    f"{f(fu['steps_per_s_median']) + (' †' if fu.get('obs_note') else '') if fu else '—'} | {b(st)} | {b(fu)} | "
                    f"{f(st.get('oracle_1core', float('nan')))} | {f(st.get('oracle_all_cores', float('nan')))} |")
@@ -58,7 +58,7 @@ def main():
     tag = sys.argv[1]
     p = os.path.join(ROOT, "BASELINE.md")
     s = open(p).read()
-    a = s.index("| Config | Game / ROM | n per GPU | Obs | Actions | Protocol | step: steps/s (IQR)")
+    a = s.index("| Config | Game / ROM | n per GPU |")
     b = s.index("\n† A fused rollout") if "\n† A fused rollout" in s else s.index("\nBool obs at 1M envs")
     s = s[:a] + table(tag) + s[b:]
     a = s.index("Headline (`bench.py`, `profiles/")
