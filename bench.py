@@ -658,37 +658,45 @@ def main():
     if not args.no_sweep and not args.no_fused:
         names = ["pong_standin", "brix_standin", "target_shooter_level1", "target_shooter_level2",
                  "target_shooter_level3"]
-        hs = []
-        for k in range(16):
-            grom, gspec = workloads.game(names[k % len(names)])
-            st_k = torch.cuda.Stream()
-            e_k = OctaxEnv(grom, gspec, 4096, 0x0C7A251001764000, env_offset=odist.shard(rank, world, 4096 * 16)[0]
-                           + 4096 * k, stream=st_k)
-            hs.append((e_k, st_k))
-        for rep in range(2):  # warm-up rollout, then the timed one
-            torch.cuda.synchronize()
-            barrier()
-            start = torch.cuda.Event(enable_timing=True)
-            start.record()
-            ends = []
-            for e_k, st_k in hs:
-                st_k.wait_event(start)
-                with torch.cuda.stream(st_k):
-                    e_k.rollout_into(100, e_k.obs, e_k.reward, e_k.done, aseed=workloads.ACTION_SEED, t0=100 * rep)
-                end = torch.cuda.Event(enable_timing=True)
-                end.record(st_k)
-                ends.append(end)
-            torch.cuda.synchronize()
-            dt = max(start.elapsed_time(end) for end in ends) / 1e3  # CUDA events: first launch to last end
-        dt = float(odist.max_over_ranks(torch.tensor([dt], dtype=torch.float64, device="cuda")).item())
-        concurrent = {"handles": 16, "envs_per_handle": 4096, "steps": 100, "mode": "fused",
-                      "steps_per_s": world * 16 * 4096 * 100 / dt,
+        rates = {}
+        # AUTO gives each 4,096-env handle the warp-per-env kernel (best for ONE such handle); 16
+        # of them together fill the GPU, where the lane-per-env kernel's throughput wins
+        for kern in ("lane", "warp"):
+            hs = []
+            for k in range(16):
+                grom, gspec = workloads.game(names[k % len(names)])
+                st_k = torch.cuda.Stream()
+                e_k = OctaxEnv(grom, gspec, 4096, 0x0C7A251001764000, env_offset=odist.shard(rank, world, 4096 * 16)[0]
+                               + 4096 * k, stream=st_k, kernel=kern)
+                hs.append((e_k, st_k))
+            for rep in range(2):  # warm-up rollout, then the timed one
+                torch.cuda.synchronize()
+                barrier()
+                start = torch.cuda.Event(enable_timing=True)
+                start.record()
+                ends = []
+                for e_k, st_k in hs:
+                    st_k.wait_event(start)
+                    with torch.cuda.stream(st_k):
+                        e_k.rollout_into(100, e_k.obs, e_k.reward, e_k.done, aseed=workloads.ACTION_SEED, t0=100 * rep)
+                    end = torch.cuda.Event(enable_timing=True)
+                    end.record(st_k)
+                    ends.append(end)
+                torch.cuda.synchronize()
+                dt = max(start.elapsed_time(end) for end in ends) / 1e3  # CUDA events: first launch to last end
+            dt = float(odist.max_over_ranks(torch.tensor([dt], dtype=torch.float64, device="cuda")).item())
+            rates[kern] = world * 16 * 4096 * 100 / dt
+            for e_k, _ in hs:
+                e_k.close()
+            torch.cuda.empty_cache()
+        concurrent = {"handles": 16, "envs_per_handle": 4096, "steps": 100, "mode": "fused", "kernel": "lane",
+                      "steps_per_s": rates["lane"], "warp_kernel_steps_per_s": rates["warp"],
                       "single_handle_steps_per_s": next((r.get("steps_per_s_fused") for r in sweep
                                                          if r.get("envs_per_gpu") == 4096), None),
+                      "note": "octax_set_kernel(LANE) on every handle: AUTO picks per handle (warp for one "
+                              "4,096-env handle); concurrent handles that together fill the GPU run faster on "
+                              "the lane-per-env kernel",
                       "timing": "CUDA events: a start event all 16 streams wait on, to the latest of their end events"}
-        for e_k, _ in hs:
-            e_k.close()
-        torch.cuda.empty_cache()
 
     # ---- per-game throughput at BASELINE configs[3]'s size (262,144 envs per GPU): the
     #      paper claims one number for all games; a SIMT interpreter is game dependent

@@ -251,7 +251,10 @@ octax_status octax_state_digests(octax_env *e, uint64_t first, uint64_t count, u
  *     divergence (the paper's lockstep bottleneck): lower latency per step, for batches
  *     too small to fill the GPU with lane-per-env warps (512..8,192 envs);
  *   OCTAX_KERNEL_AUTO -- WARP when n <= OCTAX_WARP_AUTO_MAX_ENVS (the measured crossover;
- *     environment variable OCTAX_WARP_AUTO_MAX overrides it at create), else LANE.
+ *     environment variable OCTAX_WARP_AUTO_MAX overrides it at create), else LANE.  The choice
+ *     sees only this handle: several small handles stepped concurrently on one GPU that together
+ *     exceed ~4,096 envs run faster with LANE on each (16 x 4,096 envs: 1.26e9 vs 2.9e8 env
+ *     steps/s, bench.py `concurrent_handles`). 
  * octax_set_kernel: OCTAX_E_INVALID_ARG for another value.  octax_get_kernel: the kernel in
  * use (LANE or WARP), never AUTO. */
 #define OCTAX_KERNEL_AUTO 0
