@@ -57,13 +57,13 @@ def seed_from_key(key) -> int:
 
 class OctaxGymnaxEnv:
     def __init__(self, rom: bytes, spec: dict, num_envs: int, device: int = 0, dense: bool = True,
-                 name: str = "Octax", stream=None):
+                 name: str = "Octax", stream=None, kernel: str | None = None):
         fmt = OBS_BOOL_XMAJOR if dense else OBS_PACKED
         self._spec = dict(spec, obs_format=fmt)
         self.num_envs = num_envs
         self.dense = dense
         self._name = name
-        self._env = OctaxEnv(rom, self._spec, num_envs, 0, device=device, stream=stream)
+        self._env = OctaxEnv(rom, self._spec, num_envs, 0, device=device, stream=stream, kernel=kernel)
         self._gen = 0
 
     @property

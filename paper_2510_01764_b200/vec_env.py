@@ -51,13 +51,14 @@ class Discrete:
 class OctaxVecEnv:
     def __init__(self, rom: bytes, spec: dict, num_envs: int, seed: int = 0, device: int = 0,
                  dense: bool = True, env_offset: int = 0, stream=None, stack: str = "steps",
-                 copy: bool = False):
+                 copy: bool = False, kernel: str | None = None):
         import torch
         if stack not in ("steps", "frames"):
             raise ValueError(f"stack must be 'steps' or 'frames', got {stack!r}")
         fmt = (OBS_BOOL_XMAJOR if dense else OBS_PACKED) | (OBS_STACK_FRAMES if stack == "frames" else 0)
         spec = dict(spec, obs_format=fmt)
-        self._env = OctaxEnv(rom, spec, num_envs, seed, device=device, env_offset=env_offset, stream=stream)
+        self._env = OctaxEnv(rom, spec, num_envs, seed, device=device, env_offset=env_offset, stream=stream,
+                             kernel=kernel)
         self.num_envs = num_envs
         self.dense = dense
         self.copy = copy
