@@ -23,7 +23,8 @@
  *      This deviates from SPEC S:409's "final observation, then reset before the
  *      next step": the terminal obs SPEC would return is available as
  *      octax_step_ex's final_obs_out (written for done envs).
- * Readings A1..A27 are listed in DESIGN.md.
+ * Readings A1..A33 are listed in DESIGN.md.  Two interchangeable step kernels run the
+ * step (octax_set_kernel below): one thread per env, or one warp per env for small batches.
  *
  * Memory: the library owns all VM state (device memory of the handle's device).
  * Buffers passed to octax_step / octax_reset / octax_gen_actions / octax_stats_device
