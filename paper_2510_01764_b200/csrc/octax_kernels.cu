@@ -1140,7 +1140,7 @@ struct WEnv {  // uniform per warp (replicated in every lane)
   uint32_t pc, I, sp, dt, st, halted, draw, episode, keys;
   uint64_t dirty;
   uint8_t *ram;
-  const uint8_t *img;     // p.s.image, p.s.words: kept in registers (no constant-bank reloads)
+  const uint8_t *img;     // p.s.image, p.s.words
   const uint16_t *words;
 };
 
@@ -1411,7 +1411,7 @@ octax_warp_kernel(const __grid_constant__ StepParams p, const int32_t *__restric
     W.ram = p.s.ram + env * 4096ull;
     W.img = p.s.image;
     W.words = p.s.words;
-    asm volatile("" : "+l"(W.img), "+l"(W.words));  // kept in registers, not re-read per cycle
+    asm volatile("" : "+l"(W.img), "+l"(W.words));  // (ptxas still re-reads them from the parameter bank)
     W.keys = 0;
     uint32_t v = 0, sk = 0, steps = 0, prev = 0;
     int32_t ep_ret = 0;
