@@ -1142,6 +1142,7 @@ struct WEnv {  // uniform per warp (replicated in every lane)
   uint8_t *ram;
   const uint8_t *img;     // p.s.image, p.s.words
   const uint16_t *words;
+  uint32_t quirks;        // p.quirks (read from here by the REGP instantiation)
 };
 
 // byte `a` (< 4096) of the env's memory: its HBM RAM block if written, else the pristine image.
@@ -1175,6 +1176,7 @@ __device__ __forceinline__ void w_wr(const StepParams &p, WEnv &W, int lane, boo
 #define WV(k) __shfl_sync(kFull, v, (int)(k))
 
 // one CHIP-8 instruction (oracle/octax_oracle.c cycle(), readings A15-A23)
+template <bool REGP>
 __device__ __forceinline__ void w_cycle(const StepParams &p, WEnv &W, uint32_t &v, uint32_t &sk, uint64_t &fb,
                                         int lane, uint32_t gid) {
   const uint32_t pc = W.pc;
@@ -1185,7 +1187,7 @@ __device__ __forceinline__ void w_cycle(const StepParams &p, WEnv &W, uint32_t &
   if (((W.dirty >> (pc >> 6)) & 3ull) != 0ull && pc <= 0xFFEu) op = (w_rd(p, W, pc) << 8) | w_rd(p, W, pc + 1u);
   W.pc = pc + 2u;
   const uint32_t x = (op >> 8) & 15u, y = (op >> 4) & 15u, n = op & 15u, nn = op & 255u, nnn = op & 0xFFFu;
-  const uint32_t quirks = p.quirks;
+  const uint32_t quirks = REGP ? W.quirks : p.quirks;
   switch (op >> 12) {
     case 0x0:
       if (op == 0x00E0u) {
@@ -1306,9 +1308,10 @@ __device__ __forceinline__ void w_cycle(const StepParams &p, WEnv &W, uint32_t &
 }
 
 // one 60 Hz frame: ipf instructions, then the timer tick (A1, A2); halted envs stand still
+template <bool REGP>
 __device__ __forceinline__ void w_frame(const StepParams &p, WEnv &W, uint32_t &v, uint32_t &sk, uint64_t &fb,
                                         int lane, uint32_t gid) {
-  for (uint32_t k = 0; k < p.ipf && !W.halted; ++k) w_cycle(p, W, v, sk, fb, lane, gid);
+  for (uint32_t k = 0; k < p.ipf && !W.halted; ++k) w_cycle<REGP>(p, W, v, sk, fb, lane, gid);
   if (!W.halted) {
     W.dt -= W.dt != 0u;
     W.st -= W.st != 0u;
@@ -1374,13 +1377,14 @@ __device__ __forceinline__ uint32_t w_eval(const Program &P, const StepParams &p
 }
 
 // power-on + the spec's startup segments (A11); the new episode's score baseline
+template <bool REGP>
 __device__ __forceinline__ void w_reset(const StepParams &p, WEnv &W, uint32_t &v, uint32_t &sk, uint64_t &fb,
                                         int lane, uint32_t gid, uint32_t &steps, uint32_t &prev, int32_t &ep_ret) {
   v = 0; sk = 0; fb = 0;
   W.pc = 0x200u; W.I = 0; W.sp = 0; W.dt = 0; W.st = 0; W.halted = 0; W.draw = 0; W.dirty = 0;
   for (uint32_t seg = 0; seg < p.n_startup; ++seg) {
     W.keys = p.startup_keys[seg];
-    for (uint32_t f = 0; f < p.startup_frames[seg]; ++f) w_frame(p, W, v, sk, fb, lane, gid);
+    for (uint32_t f = 0; f < p.startup_frames[seg]; ++f) w_frame<REGP>(p, W, v, sk, fb, lane, gid);
   }
   W.keys = 0;
   steps = 0;
@@ -1390,8 +1394,13 @@ __device__ __forceinline__ void w_reset(const StepParams &p, WEnv &W, uint32_t &
 
 // <= 72 registers: 28+ resident warps (envs) per SM, so 4,096 envs run in one wave on 148 SMs
 // (at 95 registers a 4,096-env step took 1.36x longer: A/B); no spills at this cap
-template <int MODE>
-__global__ void __maxnreg__(72)
+// REGP (launches of <= 2,048 envs, where the kernel is latency-bound): the image / word-table
+// pointers and the quirk bits pass through a shuffle at kernel start, which ptxas does not
+// rematerialise, so they stay in registers instead of being reloaded from the parameter bank on
+// every VM cycle (an LDC on the fetch's dependent chain): +3..6% at 512 envs; at 4,096 envs
+// (issue-bound) the plain form is 0.5..1.5% faster (A/B, profiles/r02_v43_ab_warp_variants.log)
+template <int MODE, bool REGP>
+__global__ void __maxnreg__(REGP ? 96 : 72)  // <= 2,048 envs: 14 warps per SM at most, registers are free
 octax_warp_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ actions, uint8_t *__restrict__ obs,
                   float *__restrict__ reward, uint8_t *__restrict__ done_out, uint8_t *__restrict__ term_out,
                   uint8_t *__restrict__ trunc_out) {
@@ -1409,16 +1418,22 @@ octax_warp_kernel(const __grid_constant__ StepParams p, const int32_t *__restric
     uint64_t *obs64 = reinterpret_cast<uint64_t *>(obs);
     WEnv W;
     W.ram = p.s.ram + env * 4096ull;
-    W.img = p.s.image;
-    W.words = p.s.words;
-    asm volatile("" : "+l"(W.img), "+l"(W.words));  // (ptxas still re-reads them from the parameter bank)
+    if (REGP) {
+      W.img = reinterpret_cast<const uint8_t *>(__shfl_sync(kFull, reinterpret_cast<uintptr_t>(p.s.image), 0));
+      W.words = reinterpret_cast<const uint16_t *>(__shfl_sync(kFull, reinterpret_cast<uintptr_t>(p.s.words), 0));
+      W.quirks = __shfl_sync(kFull, p.quirks, 0);
+    } else {
+      W.img = p.s.image;  // ptxas re-reads these from the parameter bank where they are used
+      W.words = p.s.words;
+      W.quirks = p.quirks;
+    }
     W.keys = 0;
     uint32_t v = 0, sk = 0, steps = 0, prev = 0;
     int32_t ep_ret = 0;
     uint64_t fb = 0, hA = 0, hB = 0;  // display (row `lane`); ends of steps t-3, t-2 (obs planes 0, 1)
     if (MODE == MODE_RESET) {
       W.episode = 0;
-      w_reset(p, W, v, sk, fb, lane, gid, steps, prev, ep_ret);
+      w_reset<REGP>(p, W, v, sk, fb, lane, gid, steps, prev, ep_ret);
       for (uint32_t sl = 0; sl < 4; ++sl) ring_at(p, sl, env)[pos] = fb;
       if (obs64)
         for (uint32_t pl = 0; pl < 4; ++pl) __stcs(obs64 + env * 128 + pl * 32 + lane, fb);
@@ -1461,7 +1476,7 @@ octax_warp_kernel(const __grid_constant__ StepParams p, const int32_t *__restric
         // last frames of this step, planes before the step's first frame = step-start display
         uint64_t P0 = sf ? start : hA, P1 = sf ? start : hB, P2 = start;
         for (uint32_t f = 0; f < p.frame_skip; ++f) {
-          w_frame(p, W, v, sk, fb, lane, gid);
+          w_frame<REGP>(p, W, v, sk, fb, lane, gid);
           const int pl = (int)f + 4 - (int)p.frame_skip;
           if (sf) {
             P0 = pl == 0 ? fb : P0;
@@ -1494,7 +1509,7 @@ octax_warp_kernel(const __grid_constant__ StepParams p, const int32_t *__restric
           ret_acc += (unsigned long long)(long long)ep_ret;
           finished++;
           W.episode++;
-          w_reset(p, W, v, sk, fb, lane, gid, steps, prev, ep_ret);  // A10: same-step auto-reset
+          w_reset<REGP>(p, W, v, sk, fb, lane, gid, steps, prev, ep_ret);  // A10: same-step auto-reset
           P0 = P1 = P2 = fb;
           for (uint32_t sl = 0; sl < 4; ++sl) ring_at(p, sl, env)[pos] = fb;
           hA = hB = fb;
@@ -1547,7 +1562,10 @@ static cudaError_t launch_warp(const StepParams &p, const int32_t *actions, uint
   const uint64_t e1 = p.block_count ? std::min<uint64_t>(p.n, e0 + (uint64_t)p.block_count * kBlock) : p.n;
   if (e1 <= e0) return cudaSuccess;
   const unsigned grid = (unsigned)((e1 - e0 + kWarpCta - 1) / kWarpCta);
-  octax_warp_kernel<MODE><<<grid, 32 * kWarpCta, 0, stream>>>(p, actions, obs, reward, done, term, trunc);
+  if (e1 - e0 <= 2048u)
+    octax_warp_kernel<MODE, true><<<grid, 32 * kWarpCta, 0, stream>>>(p, actions, obs, reward, done, term, trunc);
+  else
+    octax_warp_kernel<MODE, false><<<grid, 32 * kWarpCta, 0, stream>>>(p, actions, obs, reward, done, term, trunc);
   return cudaGetLastError();
 }
 

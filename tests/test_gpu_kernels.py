@@ -236,3 +236,17 @@ def test_config2_pong_4096_sampled_parity(monkeypatch):
         assert np.array_equal(obs.cpu().numpy().reshape(n, -1), oo), t
         assert np.array_equal(rew.cpu().numpy(), orw) and np.array_equal(done.cpu().numpy(), od), t
     P._assert_states(g, o, list(range(n)))
+
+
+@pytest.mark.parametrize("n", [2048, 2049])
+def test_warp_register_params_boundary(monkeypatch, n):
+    """The warp kernel's two instantiations (launches of <= 2,048 envs keep the image / word-table
+    pointers and quirk bits in registers; larger ones read them from the parameter bank) on
+    either side of the switch: quirks 31 and startup segments on a fuzz ROM, then a game."""
+    monkeypatch.setenv("OCTAX_KERNEL", "warp")
+    rom = workloads.gen.fuzz_rom(4242, n_instr=300)
+    spec = dict(workloads.DEFAULTS, score="V5 * 3 - VF", terminated="VE == 7", action_keys=[1, 2, 3, 12],
+                quirks=31, max_episode_steps=45, startup=[(1 << 2, 3), (0, 2)])
+    P._run_parity(rom, spec, n, 60, 11, 11, check_every=30)
+    rom, spec = workloads.game("target_shooter_level3")
+    P._run_parity(rom, spec, n, 60, 5, 5, check_every=30)
