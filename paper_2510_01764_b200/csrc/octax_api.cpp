@@ -504,7 +504,7 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   const uint64_t n = n_envs;
   size_t off = 0;
   auto carve = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
-  size_t o_img = carve(kStageBytes), o_dec = carve(8 * kDecEntries), o_words = carve(2 * kImageBytes), o_stats = carve(64), o_regs = carve(16 * n), o_ctrl = carve(16 * n),
+  size_t o_img = carve(kStageBytes), o_dec = carve(8 * kDecEntries), o_words = carve(2 * kWordEntries), o_stats = carve(64), o_regs = carve(16 * n), o_ctrl = carve(16 * n),
          o_book = carve(16 * n), o_stack = carve(32 * n), o_dirty = carve(8 * n),
          o_ring = carve(1024 * ((n + kBlock - 1) / kBlock * kBlock)),
          o_ram = carve(4096 * n);
@@ -548,11 +548,12 @@ extern "C" octax_status octax_create(const uint8_t *rom, size_t rom_len, const o
   ce = cudaMemcpyAsync(base + o_img, image, kStageBytes, cudaMemcpyHostToDevice, e->stream);
   if (ce == cudaSuccess)
     ce = cudaMemcpyAsync(base + o_dec, dec.data(), 8 * kDecEntries, cudaMemcpyHostToDevice, e->stream);
-  std::vector<uint16_t> words(kImageBytes, 0);
+  // one entry per 16-bit PC (stored PCs are 16-bit), so the warp kernel's fetch needs no clamp;
+  // every PC past 0xFFE holds 0x5001, an invalid word: the kernel halts (A17)
+  std::vector<uint16_t> words(kWordEntries, 0x5001);
   for (uint32_t pc = 0; pc < kImageBytes - 1; ++pc) words[pc] = (uint16_t)((image[pc] << 8) | image[pc + 1]);
-  words[kImageBytes - 1] = 0x5001;  // PC > 0xFFE (clamped to 0xFFF): an invalid word, the kernel halts (A17)
   if (ce == cudaSuccess)
-    ce = cudaMemcpyAsync(base + o_words, words.data(), 2 * kImageBytes, cudaMemcpyHostToDevice, e->stream);
+    ce = cudaMemcpyAsync(base + o_words, words.data(), 2 * kWordEntries, cudaMemcpyHostToDevice, e->stream);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->stream);
   if (ce != cudaSuccess) { free_env(e); return cuda_err(ce, "upload image"); }
   if (e->obs_format != OCTAX_OBS_PACKED) {

@@ -21,6 +21,7 @@ constexpr uint32_t kMaxHostChunks = OCTAX_HOST_CHUNKS;  // pipelined host steps:
 constexpr int kMaxOps = 64;
 constexpr int kMaxDepth = 8;
 constexpr uint32_t kImageBytes = 4096;
+constexpr uint32_t kWordEntries = 65536;  // warp kernel word table: one entry per 16-bit PC
 constexpr uint32_t kDescEntries = 256;
 constexpr uint32_t kStageBytes = kImageBytes + 4 * kDescEntries;  // image + decode table, one bulk copy
 

@@ -1134,6 +1134,9 @@ reset_kernel(const __grid_constant__ StepParams p, uint8_t *__restrict__ obs) {
 #ifndef OCTAX_WCTA
 #define OCTAX_WCTA 4
 #endif
+#ifndef OCTAX_WARP_PCCLAMP  // A/B knob: clamp the fetch index to 0xFFF (the table before v45 had 4,096 entries)
+#define OCTAX_WARP_PCCLAMP 0
+#endif
 constexpr int kWarpCta = OCTAX_WCTA;  // envs (warps) per CTA: small CTAs spread a small batch over all SMs
 
 struct WEnv {  // uniform per warp (replicated in every lane)
@@ -1180,10 +1183,16 @@ template <bool REGP>
 __device__ __forceinline__ void w_cycle(const StepParams &p, WEnv &W, uint32_t &v, uint32_t &sk, uint64_t &fb,
                                         int lane, uint32_t gid) {
   const uint32_t pc = W.pc;
-  // the word at PC: one load, issued first, from the pristine word table (entry 0xFFF holds
-  // 0x5001, an invalid word, so a PC past 0xFFE lands on the halting path of class 5 below);
-  // re-assembled from RAM bytes when PC's 64-B block (or the next, holding PC + 1) was written
+  // the word at PC: one load, issued first, from the pristine word table (one entry per 16-bit
+  // PC; entries past 0xFFE hold 0x5001, an invalid word, so such a PC lands on the halting path
+  // of class 5 below); re-assembled from RAM bytes when PC's 64-B block (or the next, holding
+  // PC + 1) was written
+  OCTAX_CHECK(pc < kWordEntries);
+#if OCTAX_WARP_PCCLAMP
   uint32_t op = __ldg(W.words + min(pc, 0xFFFu));
+#else
+  uint32_t op = __ldg(W.words + pc);
+#endif
   if (((W.dirty >> (pc >> 6)) & 3ull) != 0ull && pc <= 0xFFEu) op = (w_rd(p, W, pc) << 8) | w_rd(p, W, pc + 1u);
   W.pc = pc + 2u;
   const uint32_t x = (op >> 8) & 15u, y = (op >> 4) & 15u, n = op & 15u, nn = op & 255u, nnn = op & 0xFFFu;

@@ -250,3 +250,64 @@ def test_warp_register_params_boundary(monkeypatch, n):
     P._run_parity(rom, spec, n, 60, 11, 11, check_every=30)
     rom, spec = workloads.game("target_shooter_level3")
     P._run_parity(rom, spec, n, 60, 5, 5, check_every=30)
+
+
+def _idle_loop_rom() -> bytes:
+    """Delay polls (Octo's wait-delay: FX07 ; 3X00 ; 1A) with random DT, also with
+    X = F, entered at the jump back with VX != DT, and in a 64-B block made dirty by an FX55 that
+    rewrites its own bytes; a sprite draw and score between polls; a self-jump when
+    V9 reaches 6, left by truncation."""
+    w = [
+        0x6A00 | 0x05,  # 200: VA = 5
+        0xC10F,         # 202: V1 = rand & 15
+        0xF115,         # 204: DT = V1
+        0xF307,         # 206: A: V3 = DT
+        0x3300,         # 208: skip if V3 == 0
+        0x1206,         # 20A: jump A (the poll loop)
+        0xC20F,         # 20C: V2 = rand & 15
+        0xD235,         # 20E: draw 5 rows at (V2, V3) from I
+        0x7901,         # 210: V9 += 1
+        0x6307,         # 212: V3 = 7
+        0xC403,         # 214: V4 = rand & 3
+        0xF415,         # 216: DT = V4
+        0x121E,         # 218: jump to the loop's jump back (VX = 7 != DT on entry)
+        0x0000,         # 21A: (pad)
+        0xF307,         # 21C: B: V3 = DT
+        0x3300,         # 21E: skip if V3 == 0
+        0x121C,         # 220: jump B
+        0xC50F,         # 222: V5 = rand & 15
+        0xF515,         # 224: DT = V5
+        0xFF07,         # 226: C: VF = DT
+        0x3F00,         # 228: skip if VF == 0
+        0x1226,         # 22A: jump C
+        0x3906,         # 22C: skip if V9 == 6 ...
+        0x1232,         # 22E: ... else continue at 232
+        0x1230,         # 230: self-jump
+        0xA280,         # 232: I = 0x280 (a block of its own)
+        0x60F3,         # 234: V0 = 0xF3 (the byte already at 0x280)
+        0xF055,         # 236: mem[0x280] = V0 -> block 0x280 dirty, same bytes
+        0xC60F,         # 238: V6 = rand & 15
+        0xF615,         # 23A: DT = V6
+        0x1280,         # 23C: jump into the dirty block's poll loop
+    ]
+    rom = bytearray(0x100)
+    for i, x in enumerate(w):
+        rom[2 * i:2 * i + 2] = x.to_bytes(2, "big")
+    tail = [0xF307, 0x3300, 0x1280, 0x1202]  # 280: D: poll loop in the dirty block, then restart
+    for i, x in enumerate(tail):
+        rom[0x80 + 2 * i:0x80 + 2 * i + 2] = x.to_bytes(2, "big")
+    return bytes(rom)
+
+
+@pytest.mark.parametrize("ipf,fs", [(1, 1), (2, 3), (3, 4), (5, 2), (12, 4), (13, 4), (31, 7)])
+def test_idle_loop_fast_forward_parity(kernel, ipf, fs):
+    """The warp kernel's exact idle-loop fast-forward (w_cycle, 1NNN) against the oracle, which
+    executes every cycle: every remaining-cycle phase (r mod 3) across ipf, DT reaching 0 inside
+    a poll, entry at the jump back with VX != DT, X = F, a poll in a dirty RAM block (no skip),
+    a self-jump; with and without startup frames that run the same loops."""
+    rom = _idle_loop_rom()
+    spec = dict(workloads.DEFAULTS, score="V9 * 7 + V3", terminated="0", action_keys=[1, 2],
+                instructions_per_frame=ipf, frame_skip=fs, max_episode_steps=37)
+    P._run_parity(rom, spec, 67, 80, 3 + ipf, ipf, check_every=10)
+    spec["startup"] = [(0, 5)]
+    P._run_parity(rom, spec, 33, 40, 4 + ipf, ipf, check_every=10)
