@@ -32,6 +32,10 @@
  * handle's stream; those calls never synchronise the host.  Buffers passed to
  * octax_step_host, octax_stats, octax_get_state(s) and octax_set_state are host
  * buffers; those calls synchronise the handle's stream.
+ * Step / rollout / reset kernels are launched with programmatic stream serialization (PDL):
+ * the next launch's CTAs may be scheduled while the previous kernel on the stream drains, but
+ * each waits for that kernel to complete and its writes to be visible before touching any
+ * buffer, so the observable order is plain stream order.
  *
  * Layouts (per env j, local index 0..n-1):
  *   actions  int32  [n]

@@ -51,6 +51,20 @@
 namespace octax {
 
 constexpr unsigned kFull = 0xffffffffu;
+
+// Programmatic dependent launch (OCTAX_PDL): step / rollout kernels are launched with programmatic
+// stream serialization, so the next launch's CTAs are scheduled while this grid drains; each
+// waits (griddepcontrol.wait) for the preceding grid to complete and its writes to be visible
+// before touching any state, so stream order is kept exactly, only the launch gap overlaps.
+#ifndef OCTAX_PDL  // A/B knob: 0 = plain launches and no griddepcontrol instructions
+#define OCTAX_PDL 1
+#endif
+__device__ __forceinline__ void pdl_enter() {
+#if OCTAX_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 #ifndef OCTAX_LANE_DRAW_MAX
 #define OCTAX_LANE_DRAW_MAX 8
 #endif
@@ -710,6 +724,7 @@ octax_kernel(const __grid_constant__ StepParams p, const int32_t *__restrict__ a
              uint8_t *__restrict__ obs, float *__restrict__ reward, uint8_t *__restrict__ done_out,
              uint8_t *__restrict__ term_out, uint8_t *__restrict__ trunc_out) {
   extern __shared__ __align__(128) unsigned char smraw[];
+  pdl_enter();
   Smem &sm = *reinterpret_cast<Smem *>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t block0 = ((uint64_t)blockIdx.x + p.block_base) * kBlock;
@@ -1414,6 +1429,7 @@ octax_warp_kernel(const __grid_constant__ StepParams p, const int32_t *__restric
                   float *__restrict__ reward, uint8_t *__restrict__ done_out, uint8_t *__restrict__ term_out,
                   uint8_t *__restrict__ trunc_out) {
   __shared__ unsigned long long red[4][kWarpCta];
+  pdl_enter();
   const int lane = (int)(threadIdx.x & 31u), warp = (int)(threadIdx.x >> 5);
   constexpr bool kRoll = MODE == MODE_ROLLOUT || MODE == MODE_ROLLOUT_NOOBS;
   constexpr bool wobs = MODE != MODE_ROLLOUT_NOOBS;
@@ -1564,6 +1580,25 @@ octax_warp_kernel(const __grid_constant__ StepParams p, const int32_t *__restric
 }
 #undef WV
 
+// launch with programmatic stream serialization when `pdl` (and OCTAX_PDL; see pdl_enter), else a
+// plain launch (griddepcontrol.wait then returns at once)
+template <typename... A>
+static cudaError_t launch_pdl(void (*k)(A...), unsigned grid, unsigned block, size_t smem, cudaStream_t stream,
+                              bool pdl, const StepParams &p, const int32_t *actions, uint8_t *obs, float *reward,
+                              uint8_t *done, uint8_t *term, uint8_t *trunc) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (OCTAX_PDL && pdl) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, p, actions, obs, reward, done, term, trunc);
+}
+
 template <int MODE>
 static cudaError_t launch_warp(const StepParams &p, const int32_t *actions, uint8_t *obs, float *reward, uint8_t *done,
                                uint8_t *term, uint8_t *trunc, cudaStream_t stream) {
@@ -1571,11 +1606,12 @@ static cudaError_t launch_warp(const StepParams &p, const int32_t *actions, uint
   const uint64_t e1 = p.block_count ? std::min<uint64_t>(p.n, e0 + (uint64_t)p.block_count * kBlock) : p.n;
   if (e1 <= e0) return cudaSuccess;
   const unsigned grid = (unsigned)((e1 - e0 + kWarpCta - 1) / kWarpCta);
+  // PDL always: the warp kernel's batches are latency-bound (A/B: +15% at 512 envs, +1..2% at 4,096)
   if (e1 - e0 <= 2048u)
-    octax_warp_kernel<MODE, true><<<grid, 32 * kWarpCta, 0, stream>>>(p, actions, obs, reward, done, term, trunc);
-  else
-    octax_warp_kernel<MODE, false><<<grid, 32 * kWarpCta, 0, stream>>>(p, actions, obs, reward, done, term, trunc);
-  return cudaGetLastError();
+    return launch_pdl(octax_warp_kernel<MODE, true>, grid, 32 * kWarpCta, 0, stream, true, p, actions, obs, reward,
+                      done, term, trunc);
+  return launch_pdl(octax_warp_kernel<MODE, false>, grid, 32 * kWarpCta, 0, stream, true, p, actions, obs, reward,
+                    done, term, trunc);
 }
 
 // ---------------------------------------------------------------- auxiliary kernels
@@ -1716,8 +1752,15 @@ static cudaError_t launch_variant(const StepParams &p, const int32_t *actions, u
     attr_set.fetch_or(bit, std::memory_order_relaxed);
   }
   const unsigned grid = p.block_count ? p.block_count : (unsigned)((p.n + kBlock - 1) / kBlock - p.block_base);
-  octax_kernel<MODE, Q0><<<grid, kBlock, smem, stream>>>(p, actions, obs, reward, done, term, trunc);
-  return cudaGetLastError();
+  // PDL when the grid is at most one CTA per SM (latency-bound: the next launch's CTAs wait on the
+  // idle SMs) or at least one full wave (they take the slots the tail frees); a grid between the two
+  // lets the next launch's first CTAs pile onto the SMs its predecessor left half empty, which then
+  // finish last (A/B: -11% at 65,536 envs)
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool pdl = grid <= (unsigned)sms || grid >= (unsigned)sms * (unsigned)kMinBlocks;
+  return launch_pdl(octax_kernel<MODE, Q0>, grid, kBlock, smem, stream, pdl, p, actions, obs, reward, done, term,
+                    trunc);
 }
 
 template <bool Q0>
