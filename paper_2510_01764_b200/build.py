@@ -51,13 +51,16 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
 def device_code_digest(so: str = SO) -> str | None:
     """sha256 of the library's device code as `cuobjdump -sass` prints it: the identity of the
     kernels a profile was taken from (the .so file itself is not byte-reproducible across
-    builds, its SASS is).  None if cuobjdump or the library is missing."""
+    builds, its SASS is).  The fatbin's `identifier = <source paths>` header lines are left out,
+    so the same sources built in another checkout (the GPU box's scratch copy) hash the same.
+    None if cuobjdump or the library is missing."""
     import hashlib
     cuobjdump = os.path.join(os.path.dirname(NVCC), "cuobjdump")
     try:
         out = subprocess.run([cuobjdump, "-sass", so], capture_output=True, text=True, timeout=120).stdout
     except (OSError, subprocess.SubprocessError):
         return None
+    out = "".join(l for l in out.splitlines(keepends=True) if not l.lstrip().startswith("identifier ="))
     return hashlib.sha256(out.encode()).hexdigest() if out else None
 
 
