@@ -1586,6 +1586,17 @@ template <typename... A>
 static cudaError_t launch_pdl(void (*k)(A...), unsigned grid, unsigned block, size_t smem, cudaStream_t stream,
                               bool pdl, const StepParams &p, const int32_t *actions, uint8_t *obs, float *reward,
                               uint8_t *done, uint8_t *term, uint8_t *trunc) {
+  // not inside a stream capture: replayed from a CUDA graph, PDL edges measured slower (configs[1]
+  // at 4,096 envs: -8%, `profiles/r02_v46_ab_pdl.log`), and a graph has no launch gap to hide
+  if (pdl) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess) {
+      (void)cudaGetLastError();
+      pdl = false;
+    } else if (cs != cudaStreamCaptureStatusNone) {
+      pdl = false;
+    }
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
