@@ -1149,6 +1149,9 @@ reset_kernel(const __grid_constant__ StepParams p, uint8_t *__restrict__ obs) {
 #ifndef OCTAX_WCTA
 #define OCTAX_WCTA 4
 #endif
+#ifndef OCTAX_WARP_LAZY  // A/B knob: decode fields per case (1), all before the switch (0), per case above 2,048 envs (2)
+#define OCTAX_WARP_LAZY 2
+#endif
 #ifndef OCTAX_WARP_PCCLAMP  // A/B knob: clamp the fetch index to 0xFFF (the table before v45 had 4,096 entries)
 #define OCTAX_WARP_PCCLAMP 0
 #endif
@@ -1210,7 +1213,18 @@ __device__ __forceinline__ void w_cycle(const StepParams &p, WEnv &W, uint32_t &
 #endif
   if (((W.dirty >> (pc >> 6)) & 3ull) != 0ull && pc <= 0xFFEu) op = (w_rd(p, W, pc) << 8) | w_rd(p, W, pc + 1u);
   W.pc = pc + 2u;
-  const uint32_t x = (op >> 8) & 15u, y = (op >> 4) & 15u, n = op & 15u, nn = op & 255u, nnn = op & 0xFFFu;
+  // Decode fields.  Taken where a case reads them (kLazy), each case pays only for its own instead
+  // of all five before the switch: -7 instructions on the common path, +8% at 4,096 envs where the
+  // kernel is issue-bound; at <= 2,048 envs (REGP, latency-bound) they stay up front, off the
+  // dispatch's dependent chain (A/B, profiles/r02_v47_ab_warp_lazy.log)
+  constexpr bool kLazy = OCTAX_WARP_LAZY == 1 || (OCTAX_WARP_LAZY == 2 && !REGP);
+  const uint32_t x_ = kLazy ? 0u : (op >> 8) & 15u, y_ = kLazy ? 0u : (op >> 4) & 15u;
+  const uint32_t n_ = kLazy ? 0u : op & 15u, nn_ = kLazy ? 0u : op & 255u, nnn_ = kLazy ? 0u : op & 0xFFFu;
+#define x (kLazy ? ((op >> 8) & 15u) : x_)
+#define y (kLazy ? ((op >> 4) & 15u) : y_)
+#define n (kLazy ? (op & 15u) : n_)
+#define nn (kLazy ? (op & 255u) : nn_)
+#define nnn (kLazy ? (op & 0xFFFu) : nnn_)
   const uint32_t quirks = REGP ? W.quirks : p.quirks;
   switch (op >> 12) {
     case 0x0:
@@ -1330,6 +1344,12 @@ __device__ __forceinline__ void w_cycle(const StepParams &p, WEnv &W, uint32_t &
     default: __builtin_unreachable();
   }
 }
+#undef x
+#undef y
+#undef n
+#undef nn
+#undef nnn
+
 
 // one 60 Hz frame: ipf instructions, then the timer tick (A1, A2); halted envs stand still
 template <bool REGP>
