@@ -1152,6 +1152,25 @@ reset_kernel(const __grid_constant__ StepParams p, uint8_t *__restrict__ obs) {
 #ifndef OCTAX_WARP_LAZY  // A/B knob: decode fields per case (1), all before the switch (0), per case above 2,048 envs (2)
 #define OCTAX_WARP_LAZY 2
 #endif
+#ifndef OCTAX_WARP_PCHALT  // A/B knob: a fault in w_cycle marks PC bit 16 (1), sets W.halted (0), PC bit above 2,048 envs (2)
+#define OCTAX_WARP_PCHALT 2
+#endif
+template <bool REGP>
+struct WarpOpts {  // per-instantiation code shape (A/B: both win where the kernel is issue-bound, > 2,048 envs,
+                   // and lose 1..3% at <= 2,048, where it is latency-bound; profiles/r02_v47_ab_warp_*.log)
+  static constexpr bool lazy = OCTAX_WARP_LAZY == 1 || (OCTAX_WARP_LAZY == 2 && !REGP);
+  static constexpr bool pchalt = OCTAX_WARP_PCHALT == 1 || (OCTAX_WARP_PCHALT == 2 && !REGP);
+};
+// a fault: PC bit 16 marks it for w_frame (no halted flag carried through every switch case), or W.halted
+#define WHALT(pcv)                                  \
+  do {                                              \
+    if (WarpOpts<REGP>::pchalt) {                   \
+      W.pc = (pcv) | 0x10000u;                      \
+    } else {                                        \
+      W.pc = (pcv);                                 \
+      W.halted = 1;                                 \
+    }                                               \
+  } while (0)
 #ifndef OCTAX_WARP_PCCLAMP  // A/B knob: clamp the fetch index to 0xFFF (the table before v45 had 4,096 entries)
 #define OCTAX_WARP_PCCLAMP 0
 #endif
@@ -1217,7 +1236,7 @@ __device__ __forceinline__ void w_cycle(const StepParams &p, WEnv &W, uint32_t &
   // of all five before the switch: -7 instructions on the common path, +8% at 4,096 envs where the
   // kernel is issue-bound; at <= 2,048 envs (REGP, latency-bound) they stay up front, off the
   // dispatch's dependent chain (A/B, profiles/r02_v47_ab_warp_lazy.log)
-  constexpr bool kLazy = OCTAX_WARP_LAZY == 1 || (OCTAX_WARP_LAZY == 2 && !REGP);
+  constexpr bool kLazy = WarpOpts<REGP>::lazy;
   const uint32_t x_ = kLazy ? 0u : (op >> 8) & 15u, y_ = kLazy ? 0u : (op >> 4) & 15u;
   const uint32_t n_ = kLazy ? 0u : op & 15u, nn_ = kLazy ? 0u : op & 255u, nnn_ = kLazy ? 0u : op & 0xFFFu;
 #define x (kLazy ? ((op >> 8) & 15u) : x_)
@@ -1231,14 +1250,14 @@ __device__ __forceinline__ void w_cycle(const StepParams &p, WEnv &W, uint32_t &
       if (op == 0x00E0u) {
         fb = 0;
       } else if (op == 0x00EEu) {
-        if (W.sp == 0u) { W.halted = 1; return; }  // A20: stack underflow
+        if (W.sp == 0u) { WHALT(W.pc); return; }  // A20: stack underflow
         W.sp -= 1u;
         W.pc = __shfl_sync(kFull, sk, (int)W.sp);
       }
       break;  // other 0NNN: no-op (A20)
     case 0x1: W.pc = nnn; break;
     case 0x2:
-      if (W.sp == 16u) { W.halted = 1; return; }  // A20: stack overflow
+      if (W.sp == 16u) { WHALT(W.pc); return; }  // A20: stack overflow
       sk = (uint32_t)lane == W.sp ? W.pc : sk;
       W.sp += 1u;
       W.pc = nnn;
@@ -1247,8 +1266,7 @@ __device__ __forceinline__ void w_cycle(const StepParams &p, WEnv &W, uint32_t &
     case 0x4: if (WV(x) != nn) W.pc += 2u; break;
     case 0x5:
       if (n != 0u) {  // invalid word: halt with PC past it (A20); a fetch past 0xFFE: PC unchanged (A17)
-        W.halted = 1;
-        if (pc > 0xFFEu) W.pc = pc;
+        WHALT(pc > 0xFFEu ? pc : W.pc);
         return;
       }
       if (WV(x) == WV(y)) W.pc += 2u;
@@ -1269,14 +1287,14 @@ __device__ __forceinline__ void w_cycle(const StepParams &p, WEnv &W, uint32_t &
         case 0x6: r = s >> 1; f = s & 1u; break;
         case 0x7: r = b - a; f = b >= a; break;
         case 0xE: r = s << 1; f = (s >> 7) & 1u; break;
-        default: W.halted = 1; return;  // A20
+        default: WHALT(W.pc); return;  // A20
       }
       v = (uint32_t)lane == x ? (r & 255u) : v;
       if (wf) v = lane == 15 ? f : v;
       break;
     }
     case 0x9:
-      if (n != 0u) { W.halted = 1; return; }
+      if (n != 0u) { WHALT(W.pc); return; }
       if (WV(x) != WV(y)) W.pc += 2u;
       break;
     case 0xA: W.I = nnn; break;
@@ -1307,7 +1325,7 @@ __device__ __forceinline__ void w_cycle(const StepParams &p, WEnv &W, uint32_t &
       const bool down = ((W.keys >> (WV(x) & 15u)) & 1u) != 0u;  // A19
       if (nn == 0x9Eu) { if (down) W.pc += 2u; }
       else if (nn == 0xA1u) { if (!down) W.pc += 2u; }
-      else { W.halted = 1; return; }
+      else { WHALT(W.pc); return; }
       break;
     }
     case 0xF:
@@ -1338,7 +1356,7 @@ __device__ __forceinline__ void w_cycle(const StepParams &p, WEnv &W, uint32_t &
           if (quirks & 2u) W.I = (W.I + x + 1u) & 0xFFFFu;
           break;
         }
-        default: W.halted = 1; return;
+        default: WHALT(W.pc); return;
       }
       break;
     default: __builtin_unreachable();
@@ -1355,10 +1373,24 @@ __device__ __forceinline__ void w_cycle(const StepParams &p, WEnv &W, uint32_t &
 template <bool REGP>
 __device__ __forceinline__ void w_frame(const StepParams &p, WEnv &W, uint32_t &v, uint32_t &sk, uint64_t &fb,
                                         int lane, uint32_t gid) {
-  for (uint32_t k = 0; k < p.ipf && !W.halted; ++k) w_cycle<REGP>(p, W, v, sk, fb, lane, gid);
-  if (!W.halted) {
+  if (WarpOpts<REGP>::pchalt) {
+    // a fault inside the frame sets PC bit 16 (WHALT), so the loop tests PC instead of a halted
+    // flag that every switch case would otherwise have to carry
+    if (W.halted) return;
+    for (uint32_t k = 0; k < p.ipf && W.pc < 0x10000u; ++k) w_cycle<REGP>(p, W, v, sk, fb, lane, gid);
+    if (W.pc >= 0x10000u) {
+      W.pc &= 0xFFFFu;
+      W.halted = 1;
+      return;
+    }
     W.dt -= W.dt != 0u;
     W.st -= W.st != 0u;
+  } else {
+    for (uint32_t k = 0; k < p.ipf && !W.halted; ++k) w_cycle<REGP>(p, W, v, sk, fb, lane, gid);
+    if (!W.halted) {
+      W.dt -= W.dt != 0u;
+      W.st -= W.st != 0u;
+    }
   }
 }
 
