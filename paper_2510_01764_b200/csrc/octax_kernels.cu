@@ -1670,7 +1670,11 @@ static cudaError_t launch_warp(const StepParams &p, const int32_t *actions, uint
   if (e1 <= e0) return cudaSuccess;
   const unsigned grid = (unsigned)((e1 - e0 + kWarpCta - 1) / kWarpCta);
   // PDL always: the warp kernel's batches are latency-bound (A/B: +15% at 512 envs, +1..2% at 4,096)
-  if (e1 - e0 <= 2048u)
+  // the latency-bound instantiation (REGP) up to 2,048 envs for rollouts and resets, up to 1,024 for
+  // single steps: there the issue-bound one is +7..9% at 2,048 envs, a rollout -2..-3%; both lose
+  // 3..14% at 256..1,024 envs (A/B, profiles/r02_v48_ab_warp_pchalt.log run 3)
+  constexpr uint64_t kRegpMax = MODE == MODE_STEP ? 1024u : 2048u;
+  if (e1 - e0 <= kRegpMax)
     return launch_pdl(octax_warp_kernel<MODE, true>, grid, 32 * kWarpCta, 0, stream, true, p, actions, obs, reward,
                       done, term, trunc);
   return launch_pdl(octax_warp_kernel<MODE, false>, grid, 32 * kWarpCta, 0, stream, true, p, actions, obs, reward,

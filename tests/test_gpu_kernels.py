@@ -238,11 +238,13 @@ def test_config2_pong_4096_sampled_parity(monkeypatch):
     P._assert_states(g, o, list(range(n)))
 
 
-@pytest.mark.parametrize("n", [2048, 2049])
+@pytest.mark.parametrize("n", [1024, 1025, 2048, 2049])
 def test_warp_register_params_boundary(monkeypatch, n):
-    """The warp kernel's two instantiations (launches of <= 2,048 envs keep the image / word-table
-    pointers and quirk bits in registers; larger ones read them from the parameter bank) on
-    either side of the switch: quirks 31 and startup segments on a fuzz ROM, then a game."""
+    """The warp kernel's two instantiations (small launches keep the image / word-table pointers
+    and quirk bits in registers and decode up front; larger ones are shaped for issue: per-case
+    decode fields, faults in PC bit 16) on either side of the switch -- 1,024 envs for steps,
+    2,048 for rollouts: quirks 31 and startup segments on a fuzz ROM, then a game, then a
+    fused rollout with truncations."""
     monkeypatch.setenv("OCTAX_KERNEL", "warp")
     rom = workloads.gen.fuzz_rom(4242, n_instr=300)
     spec = dict(workloads.DEFAULTS, score="V5 * 3 - VF", terminated="VE == 7", action_keys=[1, 2, 3, 12],
@@ -250,6 +252,7 @@ def test_warp_register_params_boundary(monkeypatch, n):
     P._run_parity(rom, spec, n, 60, 11, 11, check_every=30)
     rom, spec = workloads.game("target_shooter_level3")
     P._run_parity(rom, spec, n, 60, 5, 5, check_every=30)
+    R.test_rollout_games_parity("target_shooter_level3", n)
 
 
 def _idle_loop_rom() -> bytes:
