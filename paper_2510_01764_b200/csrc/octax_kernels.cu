@@ -1152,6 +1152,9 @@ reset_kernel(const __grid_constant__ StepParams p, uint8_t *__restrict__ obs) {
 #ifndef OCTAX_WARP_LAZY  // A/B knob: decode fields per case (1), all before the switch (0), per case above 2,048 envs (2)
 #define OCTAX_WARP_LAZY 2
 #endif
+#ifndef OCTAX_WARP_KEXIT  // A/B knob: a fault also ends the frame loop through its counter (no per-cycle PC test)
+#define OCTAX_WARP_KEXIT 1
+#endif
 #ifndef OCTAX_WARP_PCHALT  // A/B knob: a fault in w_cycle marks PC bit 16 (1), sets W.halted (0), PC bit above 2,048 envs (2)
 #define OCTAX_WARP_PCHALT 2
 #endif
@@ -1166,6 +1169,7 @@ struct WarpOpts {  // per-instantiation code shape (A/B: both win where the kern
   do {                                              \
     if (WarpOpts<REGP>::pchalt) {                   \
       W.pc = (pcv) | 0x10000u;                      \
+      if (OCTAX_WARP_KEXIT) k = 0xFFFFFFF0u;        \
     } else {                                        \
       W.pc = (pcv);                                 \
       W.halted = 1;                                 \
@@ -1218,7 +1222,7 @@ __device__ __forceinline__ void w_wr(const StepParams &p, WEnv &W, int lane, boo
 // one CHIP-8 instruction (oracle/octax_oracle.c cycle(), readings A15-A23)
 template <bool REGP>
 __device__ __forceinline__ void w_cycle(const StepParams &p, WEnv &W, uint32_t &v, uint32_t &sk, uint64_t &fb,
-                                        int lane, uint32_t gid) {
+                                        int lane, uint32_t gid, uint32_t &k) {
   const uint32_t pc = W.pc;
   // the word at PC: one load, issued first, from the pristine word table (one entry per 16-bit
   // PC; entries past 0xFFE hold 0x5001, an invalid word, so such a PC lands on the halting path
@@ -1377,7 +1381,11 @@ __device__ __forceinline__ void w_frame(const StepParams &p, WEnv &W, uint32_t &
     // a fault inside the frame sets PC bit 16 (WHALT), so the loop tests PC instead of a halted
     // flag that every switch case would otherwise have to carry
     if (W.halted) return;
-    for (uint32_t k = 0; k < p.ipf && W.pc < 0x10000u; ++k) w_cycle<REGP>(p, W, v, sk, fb, lane, gid);
+#if OCTAX_WARP_KEXIT
+    for (uint32_t k = 0; k < p.ipf; ++k) w_cycle<REGP>(p, W, v, sk, fb, lane, gid, k);
+#else
+    for (uint32_t k = 0; k < p.ipf && W.pc < 0x10000u; ++k) w_cycle<REGP>(p, W, v, sk, fb, lane, gid, k);
+#endif
     if (W.pc >= 0x10000u) {
       W.pc &= 0xFFFFu;
       W.halted = 1;
@@ -1386,7 +1394,7 @@ __device__ __forceinline__ void w_frame(const StepParams &p, WEnv &W, uint32_t &
     W.dt -= W.dt != 0u;
     W.st -= W.st != 0u;
   } else {
-    for (uint32_t k = 0; k < p.ipf && !W.halted; ++k) w_cycle<REGP>(p, W, v, sk, fb, lane, gid);
+    for (uint32_t k = 0; k < p.ipf && !W.halted; ++k) w_cycle<REGP>(p, W, v, sk, fb, lane, gid, k);
     if (!W.halted) {
       W.dt -= W.dt != 0u;
       W.st -= W.st != 0u;
